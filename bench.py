@@ -1,0 +1,394 @@
+"""Benchmark: trajectory steps/sec (+ overlay latency) of the avalanche hot
+path on a synthetic 16384^2 DEM (BASELINE.json configs[2]), B200 vs host CPU.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = one pass of the hot path over the DEM: fused normals+steepness ->
+release_points (band 30-45 deg, stride 32) -> release ordinal compaction ->
+avalanche trajectories (2048 particles per release cell, default physics) ->
+runout invariants + stats.  Multi-GPU: the particle index space is sharded by
+release-point blocks across ranks and the private rasters are merged by an
+NCCL all-reduce (strong scaling: total work fixed).
+
+value: device-resident inputs.  e2e: the same metric through the public API
+(DemGrid from a pinned host array -> compute_normals -> steepness_deg ->
+detect_release_points -> run_avalanche -> host read of the RunoutRaster),
+host<->device copies inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "trajectory steps/sec"
+UNIT = "particle-steps/s"
+BYTES_PER_STEP = 64  # 32 B DEM patch + 16 B hit RMW + 16 B drop RMW
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", type=int, default=16384)
+    ap.add_argument("--stride", type=int, default=32)
+    ap.add_argument("--ppc", type=int, default=2048)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-chunks", type=int, default=96, help="2048-particle chunks in the CPU sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-overlay", action="store_true")
+    ap.add_argument("--overlay-size", type=int, default=8192)
+    return ap.parse_args()
+
+
+def workload(a) -> dict:
+    return {
+        "workload": f"avalanche release points + trajectories, synthetic {a.size}x{a.size} DEM (BASELINE configs[2])",
+        "dem": f"synth_dem({a.size}, seed={a.seed}, cs=10, H=300, lambda0=4000, 4 octaves)",
+        "release": f"SteepnessRelease(30, 45, stride={a.stride})",
+        "params": f"AvalancheParams(particles_per_release_cell={a.ppc}, seed={a.seed}) (defaults: p=0.9, r=0.16, alpha=25)",
+        "l2": "inputs larger than L2 (DEM 2 GiB, rasters 4 GiB per step)" if a.size >= 8192 else "small",
+    }
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[tuple[float, float, str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), ",".join(parts[3:7])))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, flags in self.samples:
+            for n, f in zip(names, flags.split(",")):
+                if f.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "src": "measured (MEASURED_PEAKS.json)", "sm_max_mhz": d.get("sm_max_mhz")}
+    return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
+
+
+# ------------------------------------------------------------------ CPU side
+
+
+def cpu_sample(elev: np.ndarray, mask: np.ndarray, a, chunks: int) -> dict:
+    """The oracle port (oracle/traj_oracle.c, the reference's engine restated
+    in C) over `chunks` evenly spaced 2048-particle chunks of the workload,
+    all host threads, bit-identical work to the GPU's for those particles."""
+    from oracle import traj
+
+    cells = np.flatnonzero(mask.ravel())
+    total = cells.size * a.ppc
+    nchunks = (total + 2047) // 2048
+    pick = np.unique(np.linspace(0, nchunks - 1, min(chunks, nchunks)).astype(np.int64))
+    threads = os.cpu_count() or 1
+    steps = 0
+    t = 0.0
+    for c in pick:
+        lo, hi = int(c) * 2048, min(int(c) * 2048 + 2048, total)
+        t0 = time.perf_counter()
+        _, h = traj.run_avalanche(elev, 0.0, 0.0, 10.0, mask, particles_per_release_cell=a.ppc, seed=a.seed,
+                                  threads=threads, lo=lo, hi=hi)
+        t += time.perf_counter() - t0
+        steps += int(h.sum()) - (hi - lo)
+    return {"value": steps / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(pick)} evenly spaced 2048-particle chunks of {nchunks} ({steps} steps, {t:.1f} s), "
+                      f"C oracle (oracle/traj_oracle.c) of the reference engine, {threads} threads",
+            "seconds": t, "steps": steps}
+
+
+def host_inputs(a):
+    from oracle import npref
+
+    from paper_2506_23364_b200.synth import synth_dem_host
+
+    e = synth_dem_host(a.size, a.seed)
+    s = npref.steepness(npref.normals(e, 10.0))
+    m = npref.release_mask(s, 30.0, 45.0, a.stride)
+    return e, m
+
+
+def run_reference(a) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    e, m = host_inputs(a)
+    vals = []
+    for i in range(a.warmup + a.steps):
+        r = cpu_sample(e, m, a, max(4, a.cpu_chunks // 4))
+        if i >= a.warmup:
+            vals.append(r)
+    v = sum(r["steps"] for r in vals) / sum(r["seconds"] for r in vals)
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "higher_is_better": True, "data": "synthetic", "dtype": "f64",
+        "config": workload(a),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "port",
+                         "sample": vals[0]["sample"] + " per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ GPU side
+
+
+def main() -> None:
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_23364_b200 as wf
+    from paper_2506_23364_b200 import _lib
+    from paper_2506_23364_b200.shard import merge_runout
+    from paper_2506_23364_b200.simulate import release_cells, run_avalanche_device
+    from paper_2506_23364_b200.synth import synth_dem_device
+    from paper_2506_23364_b200.terrain import compute_normals_and_slope
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.build()
+    L = _lib.lib()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    elev_dev = synth_dem_device(a.size, a.seed)
+    grid = wf.DemGrid(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, elev_dev)
+    params = wf.AvalancheParams(particles_per_release_cell=a.ppc, seed=a.seed)
+    traj_ms: list[float] = []
+    steps_acc = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def hot_path(g):
+        _, slope = compute_normals_and_slope(g)
+        mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
+        cells = release_cells(mask)
+        hits = torch.zeros((g.nrows, g.ncols), dtype=torch.int64, device=dev)
+        zmax = torch.zeros((g.nrows, g.ncols), dtype=torch.float64, device=dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run_avalanche_device(g, cells, params, rank=rank, nranks=world, hits=hits, zmax=zmax, steps_out=steps_acc)
+        e1.record(stream)
+        if world > 1:
+            merge_runout(hits, zmax)
+        run = wf.RunoutRaster(zmax, hits)  # invariants + stats pass
+        return run, mask, (e0, e1)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    for _ in range(a.warmup):
+        run, mask, ev = hot_path(grid)
+    released = wf.simulate.released_particles(mask, params)
+    total_steps = run.total_hits - released
+
+    # timed: device-resident
+    barrier()
+    launches0 = _lib.launch_count()
+    steps_acc.zero_()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        t0.record(stream)
+        evs = []
+        for _ in range(a.steps):
+            run, mask, ev = hot_path(grid)
+            evs.append(ev)
+        t1.record(stream)
+        barrier()
+    launches = _lib.launch_count() - launches0
+    ms = t0.elapsed_time(t1)
+    traj_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    local_steps = int(steps_acc.item()) / a.steps
+    if world > 1:
+        tt = torch.tensor([ms, max(traj_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, traj_max = tt.tolist()
+    else:
+        traj_max = max(traj_ms)
+    ms_per_step = ms / a.steps
+    value = total_steps / (ms_per_step / 1e3)
+
+    # e2e through the public API with host buffers
+    host = torch.empty((a.size, a.size), dtype=torch.float64, pin_memory=True)
+    host.copy_(elev_dev.cpu())
+    host_np = host.numpy()
+    out_h = torch.empty((a.size, a.size), dtype=torch.int64, pin_memory=True)
+    out_z = torch.empty((a.size, a.size), dtype=torch.float64, pin_memory=True)
+
+    def e2e_step():
+        g = wf.DemGrid(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, host_np)
+        slope = wf.steepness_deg(wf.compute_normals(g))
+        mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
+        r = wf.run_avalanche(g, mask, params)
+        out_h.copy_(r.dev("hit_count"), non_blocking=True)
+        out_z.copy_(r.dev("z_delta_max"), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return r
+
+    e2e_step()
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(max(1, min(a.steps, 3))):
+        e2e_step()
+    barrier()
+    e2e_n = max(1, min(a.steps, 3))
+    e2e_ms = (time.perf_counter() - w0) * 1e3 / e2e_n
+    if world > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+    e2e_value = total_steps / (e2e_ms / 1e3)
+    cell_bytes = a.size * a.size * 8
+
+    # overlay latency: full avalanche workflow through the Executor at the
+    # largest size the reference's texture cap allows (configs[3]-like)
+    overlay = None
+    if not a.no_overlay and rank == 0 and world == 1:
+        overlay = overlay_latency(wf, a)
+
+    if rank == 0:
+        pk = peaks()
+        traj_s = traj_max / 1e3
+        achieved = BYTES_PER_STEP * (local_steps if world > 1 else total_steps) / traj_s / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**workload(a), "parallelism": f"particles sharded by release-point blocks over {world} GPU(s), "
+                                                      "NCCL all-reduce of the overlay"},
+            "particle_steps_per_step": total_steps,
+            "released_particles": released,
+            "traj_kernel_ms": traj_max,
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": cell_bytes, "d2h_bytes_per_step": 2 * cell_bytes},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"],
+                         "kernel": "traj_kernel", "bytes_per_unit": BYTES_PER_STEP,
+                         "note": "algorithmic 64 B/particle-step; kernel is FP64-issue bound (see DESIGN.md)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if overlay is not None:
+            line["overlay_latency_ms"] = overlay
+        if not a.no_cpu:
+            e, m = host_inputs(a)
+            line["cpu_baseline"] = cpu_sample(e, m, a, a.cpu_chunks)
+            line["cpu_baseline"].pop("seconds")
+            line["cpu_baseline"].pop("steps")
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def overlay_latency(wf, a) -> dict:
+    """Cold and warm-steering latency of the stock avalanche graph (7 nodes)
+    on a stitched 8192^2 world (zoom 2: 16 tiles), colorize + 14-level mip."""
+    import torch
+
+    from paper_2506_23364_b200.synth import synth_dem_device
+
+    n = a.overlay_size
+    world = wf.DemGrid(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
+    rel = wf.SteepnessRelease(30.0, 45.0, stride=16)
+
+    def graph(seed):
+        g = wf.build_avalanche_graph(world.extent, wf.AvalancheParams(particles_per_release_cell=256, seed=seed),
+                                     rel, zoom=2)
+        g.bind("world", world)
+        return g
+
+    wf.Executor().execute(graph(0))  # warm the CUDA context / allocator
+    torch.cuda.synchronize()
+    cold = []
+    for s in range(2):
+        ex = wf.Executor()
+        t0 = time.perf_counter()
+        res = ex.execute(graph(s))
+        cold.append((time.perf_counter() - t0) * 1e3)
+    warm = []
+    for s in range(3):
+        t0 = time.perf_counter()
+        rep = ex.execute(graph(100 + s)).report
+        warm.append((time.perf_counter() - t0) * 1e3)
+    nodes = {r.node_id: round(r.elapsed_ms, 3) for r in res.report.records}
+    return {"config": f"stock avalanche graph, synth_dem({n}, 1) world, zoom 2 (16 tiles), band 30-45 stride 16, "
+                      "256 particles/cell, colorize + full mip",
+            "cold": min(cold), "warm_steering": min(warm), "warm_cache_hits": rep.cache_hits,
+            "stats": res.value("avalanche_overlay", "stats"), "node_ms_cold": nodes}
+
+
+if __name__ == "__main__":
+    main()
