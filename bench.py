@@ -138,20 +138,21 @@ def cpu_sample(elev: np.ndarray, mask: np.ndarray, a, chunks: int) -> dict:
     all host threads, bit-identical work to the GPU's for those particles."""
     from oracle import traj
 
-    cells = np.flatnonzero(mask.ravel())
+    cells = np.ascontiguousarray(np.flatnonzero(mask.ravel()), dtype=np.int64)
     total = cells.size * a.ppc
     nchunks = (total + 2047) // 2048
     pick = np.unique(np.linspace(0, nchunks - 1, min(chunks, nchunks)).astype(np.int64))
     threads = os.cpu_count() or 1
+    hits = np.zeros(elev.shape, dtype=np.int64)
+    zmax = np.zeros(elev.shape, dtype=np.float64)
     steps = 0
     t = 0.0
     for c in pick:
         lo, hi = int(c) * 2048, min(int(c) * 2048 + 2048, total)
         t0 = time.perf_counter()
-        _, h = traj.run_avalanche(elev, 0.0, 0.0, 10.0, mask, particles_per_release_cell=a.ppc, seed=a.seed,
-                                  threads=threads, lo=lo, hi=hi)
+        steps += traj.run_range(elev, 0.0, 0.0, 10.0, cells, lo, hi, hits, zmax, particles_per_release_cell=a.ppc,
+                                seed=a.seed, threads=threads)
         t += time.perf_counter() - t0
-        steps += int(h.sum()) - (hi - lo)
     return {"value": steps / t, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{len(pick)} evenly spaced 2048-particle chunks of {nchunks} ({steps} steps, {t:.1f} s), "
                       f"C oracle (oracle/traj_oracle.c) of the reference engine, {threads} threads",
@@ -164,8 +165,7 @@ def host_inputs(a):
     from paper_2506_23364_b200.synth import synth_dem_host
 
     e = synth_dem_host(a.size, a.seed)
-    s = npref.steepness(npref.normals(e, 10.0))
-    m = npref.release_mask(s, 30.0, 45.0, a.stride)
+    m = npref.lattice_release_mask(e, 10.0, 30.0, 45.0, a.stride)
     return e, m
 
 

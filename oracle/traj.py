@@ -87,6 +87,23 @@ def run_avalanche(elev, ox, oy, cs, mask, *, persistence=0.9, randomness=0.16, r
     return zmax, hits
 
 
+def run_range(elev, ox, oy, cs, cells, lo, hi, hits, zmax, *, persistence=0.9, randomness=0.16,
+              runout_angle_deg=25.0, particles_per_release_cell=2048, seed=0, max_steps=None, threads=None) -> int:
+    """Particles [lo, hi) accumulated into caller-owned rasters (one shared
+    pair across calls, unlike the reference's per-chunk partials); returns
+    the particle steps taken."""
+    n = hi - lo
+    if n <= 0:
+        return 0
+    steps = np.zeros(n, dtype=np.int64)
+    lib().orc_run_particles(
+        *world_args(elev, ox, oy, cs, persistence, randomness, runout_angle_deg, max_steps),
+        cells.ctypes.data, particles_per_release_cell, seed & MASK64, lo, hi, hits.ctypes.data, zmax.ctypes.data,
+        None, steps.ctypes.data, None, int(threads or os.cpu_count() or 1),
+    )
+    return int(steps.sum())
+
+
 def simulate_particle(elev, ox, oy, cs, start, key, *, persistence=0.9, randomness=0.16, runout_angle_deg=25.0,
                       max_steps=None):
     """Oracle simulate_particle (simulate.py:415-438): (positions, reason code)."""

@@ -44,6 +44,7 @@ SIGNATURES: dict[str, tuple] = {
     "wg_release_mask": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_i64, c_ptr, c_ptr]),
     "wg_compact_scratch_bytes": (c_size, [c_i64]),
     "wg_mask_compact": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "wg_avalanche_scratch_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "wg_run_avalanche": (
         c_int,
         [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_i64,
@@ -57,9 +58,10 @@ SIGNATURES: dict[str, tuple] = {
     "wg_particle_records": (
         c_int,
         [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_i64,
-         c_ptr, c_i64, c_u64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
+         c_ptr, c_i64, c_u64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     ),
     "wg_trig_eval": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
+    "wg_div_eval": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_runout_stats": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_snow": (c_int, [c_ptr, c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_int, c_dbl, c_ptr, c_ptr]),
     "wg_colorize": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr]),

@@ -340,13 +340,14 @@ def run_avalanche_device(
         hits = _device.zeros((grid.nrows, grid.ncols), torch.int64)
     if zmax is None:
         zmax = _device.zeros((grid.nrows, grid.ncols), torch.float64)
-    work = _device.zeros((2,), torch.int64)
+    scratch = _device.empty((int(L.wg_avalanche_scratch_bytes(params.particles_per_release_cell, int(i_lo),
+                                                               int(i_hi))),), torch.uint8)
     dem = grid.device_elevations()
     _lib.check(
         L.wg_run_avalanche(
             _lib.ptr(dem), *_sc_args(sc), _lib.ptr(cells), params.particles_per_release_cell,
             rng.seed_word(params.seed), int(i_lo), int(i_hi), int(shard_block), int(rank), int(nranks),
-            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(work), _lib.ptr(steps_out), _lib.stream_ptr(stream),
+            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(scratch), _lib.ptr(steps_out), _lib.stream_ptr(stream),
         ),
         ParamError,
     )
@@ -423,10 +424,13 @@ def particle_records(
     reason = _device.empty((n,), torch.int8)
     steps = _device.empty((n,), torch.int64)
     ends = _device.empty((n, 2), torch.float64)
+    scratch = _device.empty((int(L.wg_avalanche_scratch_bytes(params.particles_per_release_cell, lo, hi)),),
+                            torch.uint8)
     _lib.check(
         L.wg_particle_records(_lib.ptr(grid.device_elevations()), *_sc_args(sc), _lib.ptr(cells),
                               params.particles_per_release_cell, rng.seed_word(params.seed), int(lo), int(hi),
-                              _lib.ptr(reason), _lib.ptr(steps), _lib.ptr(ends), _lib.stream_ptr()),
+                              _lib.ptr(reason), _lib.ptr(steps), _lib.ptr(ends), _lib.ptr(scratch),
+                              _lib.stream_ptr()),
         ParamError,
     )
     return reason.cpu().numpy(), steps.cpu().numpy(), ends.cpu().numpy()
