@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--stride", type=int, default=32)
     ap.add_argument("--ppc", type=int, default=2048)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-chunks", type=int, default=96, help="2048-particle chunks in the CPU sample")
+    ap.add_argument("--cpu-chunks", type=int, default=2048, help="2048-particle chunks in the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlay", action="store_true")
     ap.add_argument("--overlay-size", type=int, default=8192)
@@ -224,7 +224,6 @@ def main() -> None:
     grid = wf.DemGrid(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, elev_dev)
     params = wf.AvalancheParams(particles_per_release_cell=a.ppc, seed=a.seed)
     traj_ms: list[float] = []
-    steps_acc = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def hot_path(g):
         _, slope = compute_normals_and_slope(g)
@@ -235,7 +234,7 @@ def main() -> None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        run_avalanche_device(g, cells, params, rank=rank, nranks=world, hits=hits, zmax=zmax, steps_out=steps_acc)
+        run_avalanche_device(g, cells, params, rank=rank, nranks=world, hits=hits, zmax=zmax)
         e1.record(stream)
         if world > 1:
             merge_runout(hits, zmax)
@@ -257,7 +256,6 @@ def main() -> None:
     # timed: device-resident
     barrier()
     launches0 = _lib.launch_count()
-    steps_acc.zero_()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -271,8 +269,19 @@ def main() -> None:
     launches = _lib.launch_count() - launches0
     ms = t0.elapsed_time(t1)
     traj_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    local_steps = int(steps_acc.item()) / a.steps
+    local_steps = total_steps
     if world > 1:
+        # this rank's share of the particle steps (for its own kernel roofline):
+        # one untimed private-raster pass, read before any merge
+        cells = release_cells(mask)
+        h = torch.zeros((a.size, a.size), dtype=torch.int64, device=dev)
+        z = torch.zeros((a.size, a.size), dtype=torch.float64, device=dev)
+        run_avalanche_device(grid, cells, params, rank=rank, nranks=world, hits=h, zmax=z)
+        from paper_2506_23364_b200.shard import local_particles
+
+        local_steps = wf.RunoutRaster(z, h).total_hits - local_particles(
+            int(cells.numel()) * a.ppc, 2048, rank, world)
+        del h, z
         tt = torch.tensor([ms, max(traj_ms)], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, traj_max = tt.tolist()

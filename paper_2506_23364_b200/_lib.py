@@ -48,7 +48,7 @@ SIGNATURES: dict[str, tuple] = {
     "wg_run_avalanche": (
         c_int,
         [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_i64,
-         c_ptr, c_i64, c_u64, c_i64, c_i64, c_i64, c_int, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+         c_ptr, c_i64, c_u64, c_i64, c_i64, c_i64, c_int, c_int, c_ptr, c_ptr, c_ptr, c_ptr],
     ),
     "wg_trace_particle": (
         c_int,

@@ -326,7 +326,6 @@ def run_avalanche_device(
     shard_block: int = _CHUNK,
     hits: torch.Tensor | None = None,
     zmax: torch.Tensor | None = None,
-    steps_out: torch.Tensor | None = None,
     stream: torch.cuda.Stream | None = None,
 ) -> tuple[torch.Tensor, torch.Tensor]:
     """Launch the trajectory kernel over particles [i_lo, i_hi) (this rank's
@@ -347,7 +346,7 @@ def run_avalanche_device(
         L.wg_run_avalanche(
             _lib.ptr(dem), *_sc_args(sc), _lib.ptr(cells), params.particles_per_release_cell,
             rng.seed_word(params.seed), int(i_lo), int(i_hi), int(shard_block), int(rank), int(nranks),
-            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(scratch), _lib.ptr(steps_out), _lib.stream_ptr(stream),
+            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(scratch), _lib.stream_ptr(stream),
         ),
         ParamError,
     )
