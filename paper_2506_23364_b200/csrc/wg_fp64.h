@@ -59,7 +59,9 @@ WG_HD double wg_copysign(double mag, double sgn) {
   return wg_from_bits((wg_bits(mag) & 0x7fffffffffffffffULL) | (wg_bits(sgn) & 0x8000000000000000ULL));
 }
 
-WG_HD double wg_neg(double x) { return wg_from_bits(wg_bits(x) ^ 0x8000000000000000ULL); }
+// IEEE negation is an exact sign flip (also for zeros); on the device it folds
+// into the consuming instruction as an operand modifier.
+WG_HD double wg_neg(double x) { return -x; }
 
 // numpy.minimum / numpy.maximum on non-NaN operands (the operands on the
 // parity paths are never NaN).  Ties return the first operand like numpy.
