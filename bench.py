@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--stride", type=int, default=32)
     ap.add_argument("--ppc", type=int, default=2048)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-chunks", type=int, default=2048, help="2048-particle chunks in the CPU sample")
+    ap.add_argument("--cpu-chunks", type=int, default=8192, help="2048-particle chunks in the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlay", action="store_true")
     ap.add_argument("--overlay-size", type=int, default=8192)

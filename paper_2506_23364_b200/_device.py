@@ -5,6 +5,8 @@ the reference's numpy attribute as a lazily materialised, read-only host view.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -18,9 +20,15 @@ def device() -> torch.device:
 
 def upload(arr: np.ndarray) -> torch.Tensor:
     """Host array -> contiguous device tensor (same dtype) on the current stream."""
+    dev = device()
     a = np.ascontiguousarray(arr)
-    t = torch.from_numpy(a) if a.size else torch.empty(a.shape, dtype=_torch_dtype(a.dtype))
-    return t.to(device(), non_blocking=True)
+    if not a.size:
+        return torch.empty(a.shape, dtype=_torch_dtype(a.dtype), device=dev)
+    with warnings.catch_warnings():
+        # read-only arrays (the frozen value types) are only read by the copy
+        warnings.simplefilter("ignore", UserWarning)
+        t = torch.from_numpy(a)
+    return t.to(dev, non_blocking=True)
 
 
 def host_view(t: torch.Tensor) -> np.ndarray:

@@ -171,6 +171,53 @@ def main() -> None:
                     "units": [drng.draw_unit(key, n) for n in (0, 1, 99)]})
     meta["rng"] = kat
 
+    # ---- the drop-in boundary: OPS port/kind tables, stock graph JSON,
+    #      validation codes of broken graphs ------------------------------------
+    from demflow import workflow as W
+
+    meta["ops"] = {
+        name: {"inputs": {p: k.value for p, k in spec.inputs.items()},
+               "outputs": {p: k.value for p, k in spec.outputs.items()}}
+        for name, spec in W.OPS.items()
+    }
+    region = d.RegionAABB(0.0, 0.0, 100.0, 50.0)
+    stock = {
+        "avalanche_mask": W.graph_to_json(W.build_avalanche_graph(
+            region, d.AvalancheParams(seed=3), W.MaskRelease(d.ReleaseMask(np.zeros((5, 10), bool))), zoom=1)),
+        "avalanche_steep": W.graph_to_json(W.build_avalanche_graph(
+            region, d.AvalancheParams(), W.SteepnessRelease(28.0, 44.0, 2), zoom=2,
+            colormap=DEFAULT_RUNOUT_COLORMAP)),
+        "snow": W.graph_to_json(W.build_snow_graph(region, d.SnowParams(snow_line_m=1200.0), zoom=0)),
+    }
+    meta["stock_graphs"] = stock
+    broken = []
+    base = W.graph_to_json(W.build_snow_graph(region, d.SnowParams(snow_line_m=1.0)))
+    import copy
+
+    def mutate(fn):
+        doc = copy.deepcopy(base)
+        fn(doc)
+        g = W.graph_from_json(doc)
+        return doc, [[v.code, v.node_id] for v in W.validate(g)]
+
+    cases = {
+        "dup": lambda doc: doc["nodes"].append(copy.deepcopy(doc["nodes"][0])),
+        "unknown_op": lambda doc: doc["nodes"][3].__setitem__("op", "nope"),
+        "unknown_node": lambda doc: doc["nodes"][4]["inputs"].__setitem__("normals", {"node": "ghost", "port": "x"}),
+        "unknown_port": lambda doc: doc["nodes"][4]["inputs"].__setitem__(
+            "normals", {"node": "surface_normals", "port": "nope"}),
+        "unknown_source": lambda doc: doc["nodes"][0]["inputs"].__setitem__("region", {"source": "nope"}),
+        "unknown_input": lambda doc: doc["nodes"][2]["inputs"].__setitem__("extra", {"source": "region"}),
+        "unbound_input": lambda doc: doc["nodes"][3]["inputs"].pop("dem"),
+        "kind_mismatch": lambda doc: doc["nodes"][4]["inputs"].__setitem__(
+            "normals", {"node": "stitch_tiles", "port": "dem"}),
+        "cycle": lambda doc: doc["nodes"][2]["inputs"].__setitem__("tiles", {"node": "stitch_tiles", "port": "dem"}),
+    }
+    for name, fn in cases.items():
+        doc, codes = mutate(fn)
+        broken.append({"name": name, "graph": doc, "violations": codes})
+    meta["broken_graphs"] = broken
+
     np.savez_compressed(OUT / "golden_arrays.npz", **arrays)
     (OUT / "golden_meta.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
     print("wrote", OUT / "golden_arrays.npz", (OUT / "golden_arrays.npz").stat().st_size, "bytes")
