@@ -11,6 +11,7 @@
 // sm_count x resident CTAs, IEEE f64 through _rn intrinsics where the
 // reference's bits must be reproduced.
 #include "wg_internal.cuh"
+#include "wg_div.cuh"
 #include "wg_fp64.h"
 
 namespace {
@@ -58,30 +59,93 @@ __device__ __forceinline__ double slope_of(double nz) {
   return WG_MUL(acos(c), 57.29577951308232);
 }
 
-// One thread per cell; neighbours come through L1/L2 (each DEM row is read
-// by three consecutive row passes of the grid-stride loop, which the 126 MB L2
-// keeps resident), so HBM traffic stays at the 8 B in + 24 B (+8 B) out floor.
-__global__ void normals_kernel(const double* __restrict__ e, int64_t nrows, int64_t ncols, double cs, double two_cs,
-                               double* __restrict__ nrm, double* __restrict__ slope) {
-  const int64_t total = nrows * ncols;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / ncols, j = t - i * ncols;
-    const double* row = e + i * ncols;
-    double dzdx, dzdy;
-    if (j == 0) dzdx = WG_DIV(WG_SUB(__ldg(row + 1), __ldg(row)), cs);
-    else if (j == ncols - 1) dzdx = WG_DIV(WG_SUB(__ldg(row + j), __ldg(row + j - 1)), cs);
-    else dzdx = WG_DIV(WG_SUB(__ldg(row + j + 1), __ldg(row + j - 1)), two_cs);
-    if (i == 0) dzdy = WG_DIV(WG_SUB(__ldg(e + j), __ldg(e + ncols + j)), cs);
-    else if (i == nrows - 1) dzdy = WG_DIV(WG_SUB(__ldg(row - ncols + j), __ldg(row + j)), cs);
-    else dzdy = WG_DIV(WG_SUB(__ldg(row - ncols + j), __ldg(row + ncols + j)), two_cs);
-    const double nx = wg_neg(dzdx), ny = wg_neg(dzdy);
-    const double len = WG_SQRT(WG_ADD(WG_ADD(WG_MUL(nx, nx), WG_MUL(ny, ny)), 1.0));
-    const double nz = WG_DIV(1.0, len);
-    double* o = nrm + 3 * t;
-    o[0] = WG_DIV(nx, len);
-    o[1] = WG_DIV(ny, len);
-    o[2] = nz;
-    if (slope != nullptr) slope[t] = slope_of(nz);
+// 2.5-D stencil: a thread owns one column of a band of kNormBand rows and
+// walks down it with a rolling (north, centre, south) register window, so
+// every DEM value is loaded once per band (+2 halo rows); east/west
+// neighbours come from warp shuffles (edge lanes load their halo).  The five
+// divisions per cell use two kernel-wide cellsize reciprocals and one shared
+// reciprocal of |n| (wg_div.cuh, __ddiv_rn-exact).  Normals are staged per
+// warp in shared memory and written as 16-byte vectors (768 contiguous bytes
+// per warp-row).  HBM floor: 8 B in + 24 B (+8 B slope) out per cell.
+constexpr int kNormBand = 64;
+constexpr int kNormThreads = 256;
+
+__global__ void __launch_bounds__(kNormThreads) normals_kernel(const double* __restrict__ e, int nrows, int ncols,
+                                                               double cs, double two_cs, double* __restrict__ nrm,
+                                                               double* __restrict__ slope) {
+  __shared__ __align__(16) double stage[kNormThreads / 32][96];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int j = blockIdx.x * kNormThreads + threadIdx.x;
+  const int jw0 = j - lane;  // first column of this warp
+  if (jw0 >= ncols) return;  // whole warp outside (warp-uniform)
+  const bool live = j < ncols;
+  const int jc = live ? j : ncols - 1;
+  const int i0 = blockIdx.y * kNormBand, i1 = min(i0 + kNormBand, nrows);
+  const double rcs = rcp_refined(cs), r2cs = rcp_refined(two_cs);
+  const bool cs_fast = b_ok(cs), c2_fast = b_ok(two_cs);
+  const double* col = e + jc;
+  double up = i0 > 0 ? __ldg(col + (size_t)(i0 - 1) * ncols) : 0.0;
+  double cur = __ldg(col + (size_t)i0 * ncols);
+  for (int i = i0; i < i1; i++) {
+    const double dn = (i + 1 < nrows) ? __ldg(col + (size_t)(i + 1) * ncols) : 0.0;
+    // east / west neighbours of row i
+    double west = __shfl_up_sync(0xffffffffu, cur, 1);
+    double east = __shfl_down_sync(0xffffffffu, cur, 1);
+    const double* row = e + (size_t)i * ncols;
+    if (lane == 0 && jc > 0) west = __ldg(row + jc - 1);
+    if ((lane == 31 || j + 1 >= ncols) && jc + 1 < ncols) east = __ldg(row + jc + 1);
+    // central differences inside, one-sided on the borders (terrain.py:79-88)
+    const bool xb = (jc == 0) | (jc == ncols - 1), yb = (i == 0) | (i == nrows - 1);
+    const double xa = WG_SUB(jc == 0 ? east : (jc == ncols - 1 ? cur : east),
+                             jc == 0 ? cur : (jc == ncols - 1 ? west : west));
+    const double ya = WG_SUB(i == 0 ? cur : up, i == 0 ? dn : (i == nrows - 1 ? cur : dn));
+    const double xd = xb ? cs : two_cs, xr = xb ? rcs : r2cs;
+    const double yd = yb ? cs : two_cs, yr = yb ? rcs : r2cs;
+    // five divisions through shared reciprocals, one guard for all of them;
+    // the rare guard miss recomputes the cell with __ddiv_rn
+    bool ok = cs_fast && c2_fast;
+    double dzdx = div_fast(xa, xd, xr, ok), dzdy = div_fast(ya, yd, yr, ok);
+    double nx = -dzdx, ny = -dzdy;
+    double len = WG_SQRT(WG_ADD(WG_ADD(WG_MUL(nx, nx), WG_MUL(ny, ny)), 1.0));
+    const double rl = rcp_refined(len);
+    ok = ok && b_ok(len);
+    double n0 = div_fast(nx, len, rl, ok);
+    double n1 = div_fast(ny, len, rl, ok);
+    double nz = div_fast(1.0, len, rl, ok);
+    if (!ok) {
+      dzdx = __ddiv_rn(xa, xd);
+      dzdy = __ddiv_rn(ya, yd);
+      nx = -dzdx;
+      ny = -dzdy;
+      len = WG_SQRT(WG_ADD(WG_ADD(WG_MUL(nx, nx), WG_MUL(ny, ny)), 1.0));
+      n0 = __ddiv_rn(nx, len);
+      n1 = __ddiv_rn(ny, len);
+      nz = __ddiv_rn(1.0, len);
+    }
+    const size_t cell = (size_t)i * ncols + j;
+    if (slope != nullptr && live) slope[cell] = slope_of(nz);
+    if (nrm != nullptr) {
+      // stage the warp's 32 x 3 doubles, then 16-byte stores when aligned
+      const size_t base = (size_t)i * ncols + jw0;  // first cell of the warp-row
+      const int nlive = min(32, ncols - jw0);
+      double* st = stage[wid];
+      st[3 * lane] = n0;
+      st[3 * lane + 1] = n1;
+      st[3 * lane + 2] = nz;
+      __syncwarp();
+      double* out = nrm + 3 * base;
+      if ((((uintptr_t)out) & 15) == 0 && nlive == 32) {
+        double2* o2 = reinterpret_cast<double2*>(out);
+        const double2* s2 = reinterpret_cast<const double2*>(st);
+        o2[lane] = s2[lane];
+        if (lane < 16) o2[32 + lane] = s2[32 + lane];
+      } else {
+        for (int q = lane; q < 3 * nlive; q += 32) out[q] = st[q];
+      }
+      __syncwarp();
+    }
+    up = cur;
+    cur = dn;
   }
 }
 
@@ -103,13 +167,37 @@ __global__ void hillshade_kernel(const double* __restrict__ nrm, int64_t n, doub
 }
 
 // ---------------------------------------------------------------- release mask
-__global__ void release_mask_kernel(const double* __restrict__ s, int64_t nrows, int64_t ncols, double lo, double hi,
-                                    int64_t stride, uint8_t* __restrict__ mask) {
-  const int64_t total = nrows * ncols;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / ncols, j = t - i * ncols;
-    const double v = __ldg(s + t);
-    mask[t] = (uint8_t)((v >= lo) & (v <= hi) & (i % stride == 0) & (j % stride == 0));
+// Each thread writes 16 mask bytes of one row (one 16-B store when aligned);
+// the slope is read only at stride-lattice cells, the only cells the mask can
+// set (simulate.py:222-225), so for stride > 1 the pass is write-bound.
+__global__ void release_mask_kernel(const double* __restrict__ s, int nrows, int ncols, double lo, double hi,
+                                    int stride, uint8_t* __restrict__ mask) {
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
+  if (c0 >= ncols) return;
+  for (int i = blockIdx.y; i < nrows; i += gridDim.y) {
+    const size_t rowoff = (size_t)i * ncols;
+    unsigned char v[16];
+    const bool lat_row = (i % stride) == 0;
+    int c = c0 % stride == 0 ? c0 : c0 + (stride - c0 % stride);
+#pragma unroll
+    for (int q = 0; q < 16; q++) v[q] = 0;
+    if (lat_row) {
+      for (; c < c0 + 16 && c < ncols; c += stride) {
+        const double x = __ldg(s + rowoff + c);
+        v[c - c0] = (unsigned char)((x >= lo) & (x <= hi));
+      }
+    }
+    uint8_t* out = mask + rowoff + c0;
+    if (c0 + 16 <= ncols && (((uintptr_t)out) & 15) == 0) {
+      uint4 w;
+      w.x = v[0] | (v[1] << 8) | (v[2] << 16) | ((unsigned)v[3] << 24);
+      w.y = v[4] | (v[5] << 8) | (v[6] << 16) | ((unsigned)v[7] << 24);
+      w.z = v[8] | (v[9] << 8) | (v[10] << 16) | ((unsigned)v[11] << 24);
+      w.w = v[12] | (v[13] << 8) | (v[14] << 16) | ((unsigned)v[15] << 24);
+      *reinterpret_cast<uint4*>(out) = w;
+    } else {
+      for (int q = 0; q < 16 && c0 + q < ncols; q++) out[q] = v[q];
+    }
   }
 }
 
@@ -291,9 +379,11 @@ int wg_copy2d_f64(const double* src, int64_t src_ld, double* dst, int64_t dst_ld
 int wg_normals(const double* elev, int64_t nrows, int64_t ncols, double cs, double two_cs, double* normals,
                double* slope, void* stream) {
   if (nrows < 2 || ncols < 2) return wg::set_error(WG_EARG, "grid must be at least 2x2");
-  if (!elev || !normals) return wg::set_error(WG_EARG, "null buffer");
-  normals_kernel<<<wg::stream_grid(nrows * ncols, kBlock), kBlock, 0, wg::as_stream(stream)>>>(elev, nrows, ncols, cs,
-                                                                                                two_cs, normals, slope);
+  if (!elev || (!normals && !slope)) return wg::set_error(WG_EARG, "null buffer");
+  if (nrows > 0x7fffffff || ncols > 0x7fffffff) return wg::set_error(WG_EARG, "grid too large");
+  const dim3 grid((unsigned)((ncols + kNormThreads - 1) / kNormThreads), (unsigned)((nrows + kNormBand - 1) / kNormBand));
+  normals_kernel<<<grid, kNormThreads, 0, wg::as_stream(stream)>>>(elev, (int)nrows, (int)ncols, cs, two_cs, normals,
+                                                                   slope);
   WG_LAUNCH_CHECK("normals_kernel");
   return WG_OK;
 }
@@ -319,8 +409,10 @@ int wg_release_mask(const double* slope, int64_t nrows, int64_t ncols, double lo
   if (stride < 1) return wg::set_error(WG_EARG, "stride must be >= 1, got %lld", (long long)stride);
   if (nrows * ncols <= 0) return WG_OK;
   if (!slope || !mask) return wg::set_error(WG_EARG, "null buffer");
-  release_mask_kernel<<<wg::stream_grid(nrows * ncols, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
-      slope, nrows, ncols, lo, hi, stride, mask);
+  if (nrows > 0x7fffffff || ncols > 0x7fffffff) return wg::set_error(WG_EARG, "grid too large");
+  const int st = stride > ncols + nrows ? (int)(ncols + nrows) : (int)stride;  // larger strides: same lattice
+  const dim3 grid((unsigned)((ncols + 16 * kBlock - 1) / (16 * kBlock)), (unsigned)(nrows < 8192 ? nrows : 8192));
+  release_mask_kernel<<<grid, kBlock, 0, wg::as_stream(stream)>>>(slope, (int)nrows, (int)ncols, lo, hi, st, mask);
   WG_LAUNCH_CHECK("release_mask_kernel");
   return WG_OK;
 }
