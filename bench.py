@@ -53,17 +53,32 @@ def parse():
     ap.add_argument("--cpu-chunks", type=int, default=8192, help="2048-particle chunks in the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlay", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", choices=["c3", "c5"], default="c3",
+                    help="c3: 16384^2 stride 32 (default, BASELINE configs[2]); "
+                         "c5: 65536^2 stride 128 seed 2 (configs[4]; slope-only prefix, no e2e/CPU legs)")
     ap.add_argument("--overlay-size", type=int, default=8192)
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.slope_only = False
+    if a.config == "c5":
+        # 65536^2: DEM 32 GiB + slope 32 GiB + rasters 64 GiB; the 96 GiB
+        # normal field would not fit next to them, so the prefix computes
+        # the slope field directly (same arithmetic, normals not stored)
+        a.size, a.stride, a.seed = 65536, 128, 2
+        a.slope_only = a.no_e2e = a.no_cpu = a.no_overlay = True
+    return a
 
 
 def workload(a) -> dict:
+    which = "configs[4], slope-only prefix" if a.config == "c5" else "configs[2]"
+    gib = a.size * a.size * 8 / 2**30
     return {
-        "workload": f"avalanche release points + trajectories, synthetic {a.size}x{a.size} DEM (BASELINE configs[2])",
+        "workload": f"avalanche release points + trajectories, synthetic {a.size}x{a.size} DEM (BASELINE {which})",
         "dem": f"synth_dem({a.size}, seed={a.seed}, cs=10, H=300, lambda0=4000, 4 octaves)",
         "release": f"SteepnessRelease(30, 45, stride={a.stride})",
         "params": f"AvalancheParams(particles_per_release_cell={a.ppc}, seed={a.seed}) (defaults: p=0.9, r=0.16, alpha=25)",
-        "l2": "inputs larger than L2 (DEM 2 GiB, rasters 4 GiB per step)" if a.size >= 8192 else "small",
+        "l2": (f"inputs larger than L2 (DEM {gib:g} GiB, rasters {2 * gib:g} GiB per step)" if a.size >= 8192
+               else "inputs may fit in L2"),
     }
 
 
@@ -207,7 +222,7 @@ def main() -> None:
     from paper_2506_23364_b200.shard import merge_runout
     from paper_2506_23364_b200.simulate import release_cells, run_avalanche_device
     from paper_2506_23364_b200.synth import synth_dem_device
-    from paper_2506_23364_b200.terrain import compute_normals_and_slope
+    from paper_2506_23364_b200.terrain import compute_normals_and_slope, compute_slope
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -226,7 +241,10 @@ def main() -> None:
     traj_ms: list[float] = []
 
     def hot_path(g):
-        _, slope = compute_normals_and_slope(g)
+        if a.slope_only:
+            slope = compute_slope(g)
+        else:
+            _, slope = compute_normals_and_slope(g)
         mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
         cells = release_cells(mask)
         hits = torch.zeros((g.nrows, g.ncols), dtype=torch.int64, device=dev)
@@ -247,8 +265,11 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up
+    # warm-up (drop the previous pass's rasters before the next allocates:
+    # at 65536^2 two generations do not fit in HBM)
+    run = mask = None
     for _ in range(a.warmup):
+        run = mask = None
         run, mask, ev = hot_path(grid)
     released = wf.simulate.released_particles(mask, params)
     total_steps = run.total_hits - released
@@ -262,6 +283,7 @@ def main() -> None:
         t0.record(stream)
         evs = []
         for _ in range(a.steps):
+            run = mask = None
             run, mask, ev = hot_path(grid)
             evs.append(ev)
         t1.record(stream)
@@ -274,6 +296,8 @@ def main() -> None:
         # this rank's share of the particle steps (for its own kernel roofline):
         # one untimed private-raster pass, read before any merge
         cells = release_cells(mask)
+        del run  # free the merged rasters first (64 GiB at 65536^2)
+        torch.cuda.empty_cache()
         h = torch.zeros((a.size, a.size), dtype=torch.int64, device=dev)
         z = torch.zeros((a.size, a.size), dtype=torch.float64, device=dev)
         run_avalanche_device(grid, cells, params, rank=rank, nranks=world, hits=h, zmax=z)
@@ -291,36 +315,38 @@ def main() -> None:
     value = total_steps / (ms_per_step / 1e3)
 
     # e2e through the public API with host buffers
-    host = torch.empty((a.size, a.size), dtype=torch.float64, pin_memory=True)
-    host.copy_(elev_dev.cpu())
-    host_np = host.numpy()
-    out_h = torch.empty((a.size, a.size), dtype=torch.int64, pin_memory=True)
-    out_z = torch.empty((a.size, a.size), dtype=torch.float64, pin_memory=True)
-
-    def e2e_step():
-        g = wf.DemGrid(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, host_np)
-        slope = wf.steepness_deg(wf.compute_normals(g))
-        mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
-        r = wf.run_avalanche(g, mask, params)
-        out_h.copy_(r.dev("hit_count"), non_blocking=True)
-        out_z.copy_(r.dev("z_delta_max"), non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return r
-
-    e2e_step()
-    barrier()
-    w0 = time.perf_counter()
-    for _ in range(max(1, min(a.steps, 3))):
-        e2e_step()
-    barrier()
-    e2e_n = max(1, min(a.steps, 3))
-    e2e_ms = (time.perf_counter() - w0) * 1e3 / e2e_n
-    if world > 1:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = tt.item()
-    e2e_value = total_steps / (e2e_ms / 1e3)
     cell_bytes = a.size * a.size * 8
+    e2e_ms = e2e_value = None
+    if not a.no_e2e:
+        host = torch.empty((a.size, a.size), dtype=torch.float64, pin_memory=True)
+        host.copy_(elev_dev.cpu())
+        out_h = torch.empty((a.size, a.size), dtype=torch.int64, pin_memory=True)
+        out_z = torch.empty((a.size, a.size), dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            g = wf.DemGrid(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, host)  # pinned host tensor
+            slope = wf.steepness_deg(wf.compute_normals(g))
+            mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
+            r = wf.run_avalanche(g, mask, params)
+            out_h.copy_(r.dev("hit_count"), non_blocking=True)
+            out_z.copy_(r.dev("z_delta_max"), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return r
+
+        e2e_step()
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(max(1, min(a.steps, 3))):
+            e2e_step()
+        barrier()
+        e2e_n = max(1, min(a.steps, 3))
+        e2e_ms = (time.perf_counter() - w0) * 1e3 / e2e_n
+        if world > 1:
+            tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = tt.item()
+        e2e_value = total_steps / (e2e_ms / 1e3)
+        del host, out_h, out_z
 
     # overlay latency: full avalanche workflow through the Executor at the
     # largest size the reference's texture cap allows (configs[3]-like)

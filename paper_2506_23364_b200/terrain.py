@@ -103,6 +103,23 @@ def compute_normals_and_slope(grid: DemGrid) -> tuple[NormalField, SlopeField]:
     return NormalField(out), SlopeField(slope)
 
 
+def compute_slope(grid: DemGrid) -> SlopeField:
+    """steepness_deg(compute_normals(grid)) in one pass without storing the
+    (nrows, ncols, 3) normal field (same per-cell arithmetic, same bits);
+    for grids whose normal field does not fit next to the rest (65536^2)."""
+    if grid.has_nodata():
+        raise TerrainError("normals require a gap-free grid (nodata present)")
+    L = _lib.lib()
+    e = grid.device_elevations()
+    slope = _device.empty((grid.nrows, grid.ncols), torch.float64)
+    cs = grid.cellsize
+    _lib.check(
+        L.wg_normals(_lib.ptr(e), grid.nrows, grid.ncols, cs, 2.0 * cs, None, _lib.ptr(slope), _lib.stream_ptr()),
+        TerrainError,
+    )
+    return SlopeField(slope)
+
+
 def steepness_deg(normals: NormalField) -> SlopeField:
     """Slope angle per cell: degrees(arccos(clip(nz))) (terrain.py:99-102)."""
     L = _lib.lib()
