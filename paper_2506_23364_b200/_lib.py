@@ -69,6 +69,7 @@ SIGNATURES: dict[str, tuple] = {
     "wg_mipmap_scratch_bytes": (c_size, [c_i64, c_i64]),
     "wg_mipmap": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_digest": (c_int, [c_ptr, c_i64, c_ptr, c_ptr]),
+    "wg_digest2d": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr]),
     "wg_synth_combine": (c_int, [c_ptr, c_ptr, c_ptr, c_int, c_i64, c_i64, c_ptr, c_ptr]),
     "wg_sub_scalar": (c_int, [c_ptr, c_i64, c_dbl, c_ptr]),
 }

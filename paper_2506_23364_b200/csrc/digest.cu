@@ -25,18 +25,26 @@ __device__ __forceinline__ unsigned long long mix(unsigned long long x) {
   return x ^ (x >> 31);
 }
 
-__global__ void digest_kernel(const unsigned char* __restrict__ data, int64_t nbytes,
+// One pass over `rows` rows of `row_bytes` bytes each, row r starting at
+// data + r*ld: chunk (r, c) is the c-th 256-byte piece of row r and is mixed
+// with its global index r*cpr + c (cpr = chunks per row), so a strided window
+// hashes exactly like the same rows stored contiguously.
+__global__ void digest_kernel(const unsigned char* __restrict__ data, int64_t rows, int64_t row_bytes, int64_t ld,
                               unsigned long long* __restrict__ out) {
-  const int64_t nchunks = (nbytes + 255) / 256;
+  const int64_t cpr = (row_bytes + 255) / 256;
+  const int64_t nchunks = rows * cpr;
   unsigned long long acc[4] = {0, 0, 0, 0};
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = c / cpr, k = c - r * cpr;
+    const unsigned char* row = data + r * ld;
+    const int64_t nbytes = row_bytes;
     unsigned long long h[4];
 #pragma unroll
     for (int l = 0; l < 4; l++) h[l] = mix(kSeeds[l] ^ ((unsigned long long)c * kGolden));
-    const int64_t base = c * 256;
-    const bool full = base + 256 <= nbytes && ((((uintptr_t)data) & 15) == 0);
+    const int64_t base = k * 256;
+    const bool full = base + 256 <= nbytes && ((((uintptr_t)(row + base)) & 15) == 0);
     if (full) {
-      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(data + base);
+      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(row + base);
 #pragma unroll 4
       for (int q = 0; q < 16; q++) {
         const ulonglong2 v = __ldg(p + q);
@@ -44,13 +52,13 @@ __global__ void digest_kernel(const unsigned char* __restrict__ data, int64_t nb
         h[(q + 1) & 3] ^= mix(v.y + kGolden * (unsigned long long)(q + 1));
       }
     } else {
-      // ragged tail: byte-wise little-endian words, zero padded, length mixed
+      // ragged or unaligned chunk: byte-wise little-endian words, zero padded
       for (int q = 0; q < 16; q++) {
         unsigned long long x = 0, y = 0;
         for (int b = 0; b < 8; b++) {
           const int64_t i0 = base + 16 * q + b, i1 = i0 + 8;
-          if (i0 < nbytes) x |= (unsigned long long)data[i0] << (8 * b);
-          if (i1 < nbytes) y |= (unsigned long long)data[i1] << (8 * b);
+          if (i0 < nbytes) x |= (unsigned long long)row[i0] << (8 * b);
+          if (i1 < nbytes) y |= (unsigned long long)row[i1] << (8 * b);
         }
         h[q & 3] = mix(h[q & 3] ^ x) + y;
         h[(q + 1) & 3] ^= mix(y + kGolden * (unsigned long long)(q + 1));
@@ -69,13 +77,19 @@ __global__ void digest_kernel(const unsigned char* __restrict__ data, int64_t nb
 
 }  // namespace
 
-extern "C" int wg_digest(const void* data, int64_t nbytes, uint64_t* out, void* stream) {
+extern "C" int wg_digest2d(const void* data, int64_t rows, int64_t row_bytes, int64_t ld_bytes, uint64_t* out,
+                           void* stream) {
   if (!out) return wg::set_error(WG_EARG, "null digest buffer");
-  if (nbytes <= 0) return WG_OK;
-  if (!data) return wg::set_error(WG_EARG, "null data");
-  const int64_t nchunks = (nbytes + 255) / 256;
+  if (rows <= 0 || row_bytes <= 0) return WG_OK;
+  if (!data || ld_bytes < row_bytes) return wg::set_error(WG_EARG, "bad digest arguments");
+  const int64_t nchunks = rows * ((row_bytes + 255) / 256);
   digest_kernel<<<wg::stream_grid(nchunks, 256, 4), 256, 0, wg::as_stream(stream)>>>(
-      reinterpret_cast<const unsigned char*>(data), nbytes, reinterpret_cast<unsigned long long*>(out));
+      reinterpret_cast<const unsigned char*>(data), rows, row_bytes, ld_bytes,
+      reinterpret_cast<unsigned long long*>(out));
   WG_LAUNCH_CHECK("digest_kernel");
   return WG_OK;
+}
+
+extern "C" int wg_digest(const void* data, int64_t nbytes, uint64_t* out, void* stream) {
+  return wg_digest2d(data, 1, nbytes, nbytes, out, stream);
 }
