@@ -38,6 +38,13 @@ sys.path.insert(0, str(ROOT))
 METRIC = "trajectory steps/sec"
 UNIT = "particle-steps/s"
 BYTES_PER_STEP = 64  # 32 B DEM patch + 16 B hit RMW + 16 B drop RMW
+# FP64-pipe instructions per particle-step (DFMA+DMUL+DADD+DSETP per active
+# thread) from the ncu SASS capture of traj_kernel (profiles/r01_traj_ncu_summary.txt),
+# and the measured FP64 instruction peak (profiles/fp64_peak.json, DADD/DMUL rate)
+FP64_OPS_PER_STEP = 173
+FP64_PEAK_OPS = 1.853e13
+# DRAM bytes per traj_kernel launch from ncu --set full (dram__bytes_read+write, r01)
+TRAJ_DRAM_BYTES = 4.12e9
 
 
 def parse():
@@ -370,9 +377,18 @@ def main() -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": cell_bytes, "d2h_bytes_per_step": 2 * cell_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"],
-                         "kernel": "traj_kernel", "bytes_per_unit": BYTES_PER_STEP,
-                         "note": "algorithmic 64 B/particle-step; kernel is FP64-issue bound (see DESIGN.md)"},
+                         "frac": achieved / pk["hbm_gbs"],
+                         "traffic": TRAJ_DRAM_BYTES if a.config == "c3" and world == 1 else None,
+                         "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r01); the gather and "
+                                         "atomics are served by the 126 MB L2",
+                         "peak_src": pk["src"], "kernel": "traj_kernel", "bytes_per_unit": BYTES_PER_STEP,
+                         "note": "algorithmic 64 B/particle-step; the binding pipe is FP64 (roofline_fp64)"},
+            "roofline_fp64": {"achieved": FP64_OPS_PER_STEP * (local_steps if world > 1 else total_steps) / traj_s,
+                              "peak": FP64_PEAK_OPS, "unit": "FP64 instr/s",
+                              "frac": FP64_OPS_PER_STEP * (local_steps if world > 1 else total_steps) / traj_s
+                              / FP64_PEAK_OPS,
+                              "ops_per_unit": FP64_OPS_PER_STEP,
+                              "peak_src": "measured DADD rate, tools/micro/fp64_peak.cu (profiles/fp64_peak.json)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
