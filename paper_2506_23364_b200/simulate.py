@@ -314,6 +314,22 @@ def _world() -> tuple[int, int]:
     return 0, 1
 
 
+def build_quad(grid: DemGrid) -> torch.Tensor | None:
+    """Patch-corner layout of the DEM (wg_build_quad: 32 B per cell, four
+    times the DEM) so every particle step gathers its bilinear patch with one
+    256-bit load; None when it would not fit comfortably (the kernel then
+    gathers from the plain DEM, same results)."""
+    need = grid.nrows * grid.ncols * 32
+    free, _ = torch.cuda.mem_get_info()
+    if need > free // 2:
+        return None
+    L = _lib.lib()
+    quad = _device.empty((grid.nrows * grid.ncols * 4,), torch.float64)
+    _lib.check(L.wg_build_quad(_lib.ptr(grid.device_elevations()), grid.nrows, grid.ncols, _lib.ptr(quad),
+                               _lib.stream_ptr()), ParamError)
+    return quad
+
+
 def run_avalanche_device(
     grid: DemGrid,
     cells: torch.Tensor,
@@ -342,9 +358,10 @@ def run_avalanche_device(
     scratch = _device.empty((int(L.wg_avalanche_scratch_bytes(params.particles_per_release_cell, int(i_lo),
                                                                int(i_hi))),), torch.uint8)
     dem = grid.device_elevations()
+    quad = build_quad(grid) if int(i_hi) > int(i_lo) else None
     _lib.check(
         L.wg_run_avalanche(
-            _lib.ptr(dem), *_sc_args(sc), _lib.ptr(cells), params.particles_per_release_cell,
+            _lib.ptr(dem), _lib.ptr(quad), *_sc_args(sc), _lib.ptr(cells), params.particles_per_release_cell,
             rng.seed_word(params.seed), int(i_lo), int(i_hi), int(shard_block), int(rank), int(nranks),
             _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(scratch), _lib.stream_ptr(stream),
         ),

@@ -66,3 +66,19 @@ for src, t in sorted(agg_t.items(), key=lambda kv: -kv[1])[:top]:
     f, n = src if src else ("?", 0)
     text = src_lines.get(f, [""] * (n + 1))[n - 1].strip() if f in src_lines and n else ""
     print(f"{f}:{n:<12d} {t / T * 100:9.2f} {agg_s[src] / S * 100:7.2f}  {text[:80]}")
+
+# per-line opcode breakdown for the hottest lines (set OPS=1)
+import os
+if os.environ.get("OPS"):
+    per = collections.defaultdict(collections.Counter)
+    ii = hdr.index("Instructions Executed")
+    for x in v:
+        off = int(x[0], 16) - base
+        src = line_of.get(off, (("?", 0), ""))[0]
+        toks = x[1].split()
+        op = toks[1] if toks and toks[0].startswith("@") and len(toks) > 1 else (toks[0] if toks else "")
+        per[src][op.split(".")[0]] += float(x[ii] or 0)
+    W = sum(sum(c.values()) for c in per.values())
+    for src, t in sorted(agg_t.items(), key=lambda kv: -kv[1])[:top]:
+        c = per[src]
+        print(f"{src[0]}:{src[1]}", ", ".join(f"{o} {n / W * 100:.2f}" for o, n in c.most_common(6)))
