@@ -63,6 +63,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "wg_trig_eval": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_div_eval": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
+    "wg_sqrt_eval": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_runout_stats": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_snow": (c_int, [c_ptr, c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_int, c_dbl, c_ptr, c_ptr]),
     "wg_colorize": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr]),
