@@ -42,7 +42,8 @@ class Nvml:
                 c = self.n.nvmlDeviceGetClockInfo(self.h, self.n.NVML_CLOCK_SM)
                 r = self.n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 p = self.n.nvmlDeviceGetPowerUsage(self.h)
-                self.samples.append((c, r, p))
+                t = self.n.nvmlDeviceGetTemperature(self.h, self.n.NVML_TEMPERATURE_GPU)
+                self.samples.append((c, r, p, t))
                 time.sleep(0.005)
 
         self.t = self.threading.Thread(target=run, daemon=True)
@@ -56,12 +57,14 @@ class Nvml:
     def summary(self):
         if not self.samples:
             return {}
-        cl = sorted(c for c, _, _ in self.samples)
+        cl = sorted(c for c, _, _, _ in self.samples)
         reasons = 0
-        for _, r, _ in self.samples:
+        for _, r, _, _ in self.samples:
             reasons |= r
+        pw = [p for _, _, p, _ in self.samples]
         return {"mhz_min": cl[0], "mhz_med": cl[len(cl) // 2], "reasons": hex(reasons),
-                "w_max": max(p for _, _, p in self.samples) // 1000}
+                "w_max": max(pw) // 1000, "w_mean": sum(pw) // len(pw) // 1000,
+                "temp_max": max(t for _, _, _, t in self.samples)}
 
 
 def main():
