@@ -38,6 +38,28 @@ def host_view(t: torch.Tensor) -> np.ndarray:
     return a
 
 
+_peek_bufs: dict[int, torch.Tensor] = {}
+
+
+def read_small(t: torch.Tensor) -> list:
+    """Values of a small 8-byte-element device tensor (counters, stats) as a
+    Python list, synchronising only the current stream.  Read through
+    wg_peek (SM stores into pinned host memory), so it never waits behind a
+    large device-to-host copy another stream has queued on the copy engine."""
+    assert t.is_cuda and t.element_size() == 8 and t.numel() <= 1024
+    src = t.contiguous()
+    stream = torch.cuda.current_stream()
+    key = stream.cuda_stream
+    buf = _peek_bufs.get(key)
+    if buf is None:
+        buf = torch.empty(1024, dtype=torch.int64, pin_memory=True)
+        _peek_bufs[key] = buf
+    L = _lib.lib()
+    _lib.check(L.wg_peek(_lib.ptr(src), _lib.ptr(buf), src.numel(), _lib.stream_ptr(stream)))
+    stream.synchronize()
+    return buf[: src.numel()].view(src.dtype).tolist()
+
+
 def empty(shape, dtype: torch.dtype) -> torch.Tensor:
     return torch.empty(shape, dtype=dtype, device=device())
 

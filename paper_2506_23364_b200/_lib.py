@@ -36,6 +36,7 @@ SIGNATURES: dict[str, tuple] = {
     "wg_version": (ctypes.c_char_p, []),
     "wg_launch_count": (c_u64, []),
     "wg_device_sms": (c_int, [ctypes.POINTER(c_int)]),
+    "wg_peek": (c_int, [c_ptr, c_ptr, c_i64, c_ptr]),
     "wg_grid_scan": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_ptr]),
     "wg_copy2d_f64": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr]),
     "wg_normals": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr]),

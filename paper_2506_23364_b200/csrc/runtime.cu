@@ -38,6 +38,16 @@ int sm_count() {
 
 }  // namespace wg
 
+namespace {
+// Small device -> host readback written by the SMs straight into pinned
+// (UVA-mapped) host memory: it does not queue behind bulk transfers on the
+// device-to-host copy engine.
+__global__ void peek_kernel(const unsigned long long* __restrict__ src, unsigned long long* dst, int n) {
+  const int i = threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+}  // namespace
+
 extern "C" {
 
 const char* wg_last_error(void) { return g_err; }
@@ -50,6 +60,17 @@ int wg_device_sms(int* sms) {
   int dev = 0;
   WG_CUDA_TRY(cudaGetDevice(&dev));
   WG_CUDA_TRY(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+  return WG_OK;
+}
+
+int wg_peek(const void* src, void* host_dst, int64_t nwords, void* stream) {
+  if (nwords <= 0) return WG_OK;
+  if (nwords > 1024) return wg::set_error(WG_EARG, "wg_peek reads at most 1024 words");
+  if (!src || !host_dst) return wg::set_error(WG_EARG, "null buffer");
+  if ((((uintptr_t)src) | ((uintptr_t)host_dst)) & 7) return wg::set_error(WG_EARG, "buffers must be 8-byte aligned");
+  peek_kernel<<<1, 1024, 0, wg::as_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(src),
+                                                     reinterpret_cast<unsigned long long*>(host_dst), (int)nwords);
+  WG_LAUNCH_CHECK("peek_kernel");
   return WG_OK;
 }
 

@@ -123,7 +123,7 @@ class ReleaseMask(Resident):
     def count(self) -> int:
         if self._count is None:
             if self.on_device("mask"):
-                object.__setattr__(self, "_count", int(self.dev("mask").sum().item()))
+                object.__setattr__(self, "_count", int(_device.read_small(self.dev("mask").sum(dtype=torch.int64).reshape(1))[0]))
             else:
                 object.__setattr__(self, "_count", int(self._h["mask"].sum()))
         return self._count
@@ -143,16 +143,22 @@ class RunoutRaster(Resident):
         "hit_count": (np.dtype(np.int64), torch.int64),
     }
 
-    def __init__(self, z_delta_max, hit_count, *, _stats: tuple[int, int, float] | None = None):
+    def __init__(self, z_delta_max, hit_count, *, _stats: tuple[int, int, float] | None = None,
+                 _deferred: bool = False):
         zs = tuple(z_delta_max.shape) if isinstance(z_delta_max, torch.Tensor) else np.shape(z_delta_max)
         hs = tuple(hit_count.shape) if isinstance(hit_count, torch.Tensor) else np.shape(hit_count)
         if tuple(zs) != tuple(hs):
             raise SimulationError(f"layer shapes differ: {tuple(zs)} vs {tuple(hs)}")
         super().__init__(z_delta_max=z_delta_max, hit_count=hit_count)
         object.__setattr__(self, "_stats", _stats)
-        self._validate()
+        object.__setattr__(self, "_stats_dev", None)
+        self._validate(_deferred)
 
-    def _validate(self) -> None:
+    def _validate(self, deferred: bool = False) -> None:
+        """``deferred`` (rasters the trajectory kernel just wrote, whose
+        invariants hold by construction): launch the stats pass and read it
+        back only when a stat is first used, so the host does not wait for
+        the simulation here."""
         if self._stats is not None:
             return
         if not (self.on_device("z_delta_max") or torch.cuda.is_available()):
@@ -165,7 +171,15 @@ class RunoutRaster(Resident):
         out = torch.zeros(4, dtype=torch.int64, device=z.device)
         _lib.check(L.wg_runout_stats(_lib.ptr(h), _lib.ptr(z), z.numel(), _lib.ptr(out), _lib.stream_ptr()),
                    SimulationError)
-        s, nnz, zbits, bad = out.tolist()
+        if deferred:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            object.__setattr__(self, "_stats_dev", (out, ev))
+            return
+        self._resolve(out)
+
+    def _resolve(self, out: torch.Tensor) -> None:
+        s, nnz, zbits, bad = _device.read_small(out)
         if bad:
             # reproduce the reference's specific message
             self._check_host(self.z_delta_max, self.hit_count)
@@ -190,17 +204,25 @@ class RunoutRaster(Resident):
     def ncols(self) -> int:
         return self.shape_of("z_delta_max")[1]
 
+    def _stat(self, i: int):
+        if self._stats is None:
+            out, ev = self._stats_dev
+            ev.synchronize()  # the stats pass may have run on another stream
+            self._resolve(out)
+            object.__setattr__(self, "_stats_dev", None)
+        return self._stats[i]
+
     @property
     def total_hits(self) -> int:
-        return self._stats[0]
+        return self._stat(0)
 
     @property
     def cells_hit(self) -> int:
-        return self._stats[1]
+        return self._stat(1)
 
     @property
     def z_max(self) -> float:
-        return self._stats[2]
+        return self._stat(2)
 
     def __repr__(self) -> str:
         return f"RunoutRaster({self.nrows}x{self.ncols})"
@@ -302,7 +324,7 @@ def release_cells(mask: ReleaseMask) -> torch.Tensor:
     scratch = _device.empty((int(L.wg_compact_scratch_bytes(n)),), torch.uint8)
     _lib.check(L.wg_mask_compact(_lib.ptr(m), n, _lib.ptr(cells), _lib.ptr(count), _lib.ptr(scratch),
                                  _lib.stream_ptr()))
-    k = int(count.item())
+    k = int(_device.read_small(count.reshape(-1)[:1])[0])
     return cells[:k]
 
 
@@ -391,14 +413,14 @@ def run_avalanche(
     hits = _device.zeros((grid.nrows, grid.ncols), torch.int64)
     zmax = _device.zeros((grid.nrows, grid.ncols), torch.float64)
     if cells.numel() == 0:
-        return RunoutRaster(zmax, hits)
+        return RunoutRaster(zmax, hits, _deferred=True)
     rank, world = _world()
     run_avalanche_device(grid, cells, params, rank=rank, nranks=world, hits=hits, zmax=zmax)
     if world > 1:
         from .shard import merge_runout
 
         merge_runout(hits, zmax)
-    return RunoutRaster(zmax, hits)
+    return RunoutRaster(zmax, hits, _deferred=True)
 
 
 def simulate_particle(
