@@ -1,0 +1,276 @@
+// ESRI ASCII grid reader/writer on the device:
+// /root/reference/pkg/src/demflow/asciigrid.py -- parse_ascii_grid (42-143)
+// tokenises the body with str.split() and converts every token with
+// np.array(tokens, dtype=float64); write_ascii_grid (146-157) joins
+// format_number(v) (160-167) with single spaces, one raster row per line.
+//
+// Reader: (1) tokenise -- one pass over the body marks token starts (a
+// non-whitespace byte after whitespace; str.split()'s ASCII whitespace is
+// \t \n \v \f \r \x1c-\x1f and space), per-4-KiB-tile counts, a scan of the
+// tile counts, and a scatter of the start offsets; (2) parse -- one thread per
+// token runs nc_parse (wg_numconv.cuh: CPython float() semantics, correctly
+// rounded) and records the first invalid token.  Writer: one thread per value
+// runs nc_format (format_number: int digits or shortest round-trip repr);
+// pass 1 sums the formatted lengths per block, a scan places the blocks,
+// pass 2 formats again into shared memory and streams each block's bytes out.
+#include "wg_internal.cuh"
+
+#define NC_TABLE __device__ const
+#include "pow5_tables.inc"
+#include "wg_numconv.cuh"
+
+namespace {
+
+constexpr int kTokThreads = 256;
+constexpr int kTokBytes = 16;  // per thread
+constexpr int64_t kTokTile = (int64_t)kTokThreads * kTokBytes;
+constexpr int kFmtThreads = 256;
+constexpr int kFmtMax = 25;  // longest format_number output (24) + separator
+
+__device__ __forceinline__ bool is_ws(unsigned c) { return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f); }
+
+// token-start bits of this thread's 16 bytes [p0, p0 + 16) within [lo, n)
+__device__ __forceinline__ unsigned start_bits(const unsigned char* __restrict__ t, int64_t p0, int64_t lo, int64_t n,
+                                               unsigned& nonascii) {
+  unsigned char b[kTokBytes];
+  if (p0 + kTokBytes <= n && ((reinterpret_cast<uintptr_t>(t + p0) & 15) == 0)) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(t + p0));
+    *reinterpret_cast<uint4*>(b) = v;
+  } else {
+    for (int k = 0; k < kTokBytes; k++) b[k] = (p0 + k < n) ? __ldg(t + p0 + k) : ' ';
+  }
+  unsigned prev_ws = (p0 <= lo) ? 1u : (is_ws(__ldg(t + p0 - 1)) ? 1u : 0u);
+  unsigned bits = 0;
+  for (int k = 0; k < kTokBytes; k++) {
+    const unsigned c = b[k];
+    const bool in = p0 + k >= lo && p0 + k < n;
+    const bool ws = is_ws(c);
+    if (in && !ws && prev_ws) bits |= 1u << k;
+    if (in) nonascii |= c >> 7;
+    prev_ws = ws ? 1u : 0u;
+  }
+  return bits;
+}
+
+__global__ void tok_count_kernel(const unsigned char* __restrict__ t, int64_t lo, int64_t n,
+                                 unsigned long long* __restrict__ tile_counts, unsigned* __restrict__ flags) {
+  const int64_t p0 = (int64_t)blockIdx.x * kTokTile + (int64_t)threadIdx.x * kTokBytes;
+  unsigned nonascii = 0;
+  const unsigned bits = start_bits(t, p0, lo, n, nonascii);
+  unsigned c = __popc(bits);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ unsigned s[kTokThreads / 32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  if (__any_sync(0xffffffffu, nonascii) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < kTokThreads / 32; w++) tot += s[w];
+    tile_counts[blockIdx.x] = tot;
+  }
+}
+
+// exclusive scan of n counts in place (one block); total to *total
+__global__ void scan_kernel(unsigned long long* __restrict__ v, int64_t n, unsigned long long* __restrict__ total) {
+  __shared__ unsigned long long s[1024];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const unsigned long long x = i < n ? v[i] : 0;
+    s[threadIdx.x] = x;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const unsigned long long y = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
+      __syncthreads();
+      s[threadIdx.x] += y;
+      __syncthreads();
+    }
+    if (i < n) v[i] = carry + s[threadIdx.x] - x;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += s[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void tok_scatter_kernel(const unsigned char* __restrict__ t, int64_t lo, int64_t n,
+                                   const unsigned long long* __restrict__ tile_offsets, int64_t* __restrict__ starts,
+                                   int64_t cap, int64_t base) {
+  const int64_t p0 = (int64_t)blockIdx.x * kTokTile + (int64_t)threadIdx.x * kTokBytes;
+  unsigned dummy = 0;
+  unsigned bits = start_bits(t, p0, lo, n, dummy);
+  const unsigned c = __popc(bits);
+  // block exclusive scan of c
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __shared__ unsigned ws[kTokThreads / 32];
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  unsigned woff = 0;
+  for (int w = 0; w < warp; w++) woff += ws[w];
+  int64_t idx = (int64_t)tile_offsets[blockIdx.x] + woff + x - c;
+  while (bits) {
+    const int k = __ffs(bits) - 1;
+    bits &= bits - 1;
+    if (idx < cap) starts[idx] = base + p0 + k;
+    idx++;
+  }
+}
+
+__global__ void parse_kernel(const unsigned char* __restrict__ t, int64_t n, const int64_t* __restrict__ starts,
+                             int64_t count, double* __restrict__ out, unsigned long long* __restrict__ first_bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = starts[i];
+    int64_t e = s;
+    while (e < n && !is_ws(__ldg(t + e))) e++;
+    const int64_t len = e - s;
+    double v = 0.0;
+    const int rc = len > 0x7fffffff ? -1 : nc::nc_parse(t + s, (int)len, &v, (const uint64_t(*)[2])kEL);
+    if (rc != 0) atomicMin(first_bad, (unsigned long long)i);
+    out[i] = v;
+  }
+}
+
+__device__ __forceinline__ int format_value(double v, char* buf) {
+  return nc::nc_format(v, buf, (const uint64_t(*)[2])kPow5Inv, (const uint64_t(*)[2])kPow5);
+}
+
+// pass 1: bytes per block of kFmtThreads values (value + separator)
+__global__ void fmt_len_kernel(const double* __restrict__ v, int64_t count, unsigned long long* __restrict__ block_bytes) {
+  const int64_t i = (int64_t)blockIdx.x * kFmtThreads + threadIdx.x;
+  char buf[32];
+  unsigned len = 0;
+  if (i < count) len = (unsigned)format_value(v[i], buf) + 1;
+  for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
+  __shared__ unsigned s[kFmtThreads / 32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = len;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < kFmtThreads / 32; w++) tot += s[w];
+    block_bytes[blockIdx.x] = tot;
+  }
+}
+
+// pass 2: format into shared memory at the block-local offsets, then copy
+// the block's contiguous bytes to out + block offset
+__global__ void fmt_write_kernel(const double* __restrict__ v, int64_t count, int64_t cols,
+                                 const unsigned long long* __restrict__ block_offsets, unsigned char* __restrict__ out) {
+  __shared__ unsigned char stage[kFmtThreads * kFmtMax];
+  __shared__ unsigned ws[kFmtThreads / 32];
+  const int64_t i = (int64_t)blockIdx.x * kFmtThreads + threadIdx.x;
+  char buf[32];
+  unsigned len = 0;
+  if (i < count) {
+    len = (unsigned)format_value(v[i], buf);
+    buf[len] = (i % cols == cols - 1) ? '\n' : ' ';
+    len += 1;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned x = len;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  unsigned woff = 0, total = 0;
+  for (int w = 0; w < kFmtThreads / 32; w++) {
+    if (w < warp) woff += ws[w];
+    total += ws[w];
+  }
+  const unsigned off = woff + x - len;
+  for (unsigned k = 0; k < len; k++) stage[off + k] = (unsigned char)buf[k];
+  __syncthreads();
+  unsigned char* dst = out + block_offsets[blockIdx.x];
+  for (unsigned k = threadIdx.x; k < total; k += kFmtThreads) dst[k] = stage[k];
+}
+
+int64_t ntiles_of(int64_t n) { return (n + kTokTile - 1) / kTokTile; }
+
+}  // namespace
+
+extern "C" {
+
+size_t wg_ascii_tokenize_scratch_bytes(int64_t n) { return 256 + (size_t)(ntiles_of(n) + 1) * 8; }
+
+int wg_ascii_tokenize(const uint8_t* text, int64_t n, int64_t body_off, int64_t* starts, int64_t cap,
+                      uint64_t* count_flags, void* scratch, void* stream) {
+  if (n < 0 || body_off < 0 || body_off > n || cap < 0) return wg::set_error(WG_EARG, "bad text range");
+  if (!count_flags || !scratch || (n > 0 && !text) || (cap > 0 && !starts)) return wg::set_error(WG_EARG, "null buffer");
+  cudaStream_t st = wg::as_stream(stream);
+  // count_flags[0] = number of tokens, count_flags[1] = 1 if a byte >= 0x80
+  WG_CUDA_TRY(cudaMemsetAsync(count_flags, 0, 2 * sizeof(uint64_t), st));
+  if (n == body_off) return WG_OK;
+  const int64_t first_tile = body_off / kTokTile;
+  const int64_t tiles = ntiles_of(n) - first_tile;
+  unsigned long long* tile = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(scratch) + 256);
+  // tiles are indexed from the body's first tile: shift the text base
+  const unsigned char* t0 = text + first_tile * kTokTile;
+  const int64_t lo = body_off - first_tile * kTokTile, len = n - first_tile * kTokTile;
+  if (tiles > 0x7fffffff) return wg::set_error(WG_ELIMIT, "text too large");
+  tok_count_kernel<<<(unsigned)tiles, kTokThreads, 0, st>>>(t0, lo, len, tile,
+                                                            reinterpret_cast<unsigned*>(count_flags + 1));
+  WG_LAUNCH_CHECK("tok_count_kernel");
+  scan_kernel<<<1, 1024, 0, st>>>(tile, tiles, reinterpret_cast<unsigned long long*>(count_flags));
+  WG_LAUNCH_CHECK("scan_kernel");
+  if (cap > 0) {
+    tok_scatter_kernel<<<(unsigned)tiles, kTokThreads, 0, st>>>(t0, lo, len, tile, starts, cap,
+                                                                first_tile * kTokTile);
+    WG_LAUNCH_CHECK("tok_scatter_kernel");
+  }
+  return WG_OK;
+}
+
+int wg_ascii_parse(const uint8_t* text, int64_t n, const int64_t* starts, int64_t count, double* out,
+                   uint64_t* first_bad, void* stream) {
+  if (n < 0 || count < 0) return wg::set_error(WG_EARG, "bad text range");
+  if (!first_bad || (count > 0 && (!text || !starts || !out))) return wg::set_error(WG_EARG, "null buffer");
+  cudaStream_t st = wg::as_stream(stream);
+  WG_CUDA_TRY(cudaMemsetAsync(first_bad, 0xff, sizeof(uint64_t), st));
+  if (count == 0) return WG_OK;
+  parse_kernel<<<wg::stream_grid(count, 256, 8), 256, 0, st>>>(text, n, starts, count, out,
+                                                               reinterpret_cast<unsigned long long*>(first_bad));
+  WG_LAUNCH_CHECK("parse_kernel");
+  return WG_OK;
+}
+
+size_t wg_ascii_format_scratch_bytes(int64_t count) {
+  return 256 + (size_t)((count + kFmtThreads - 1) / kFmtThreads + 1) * 8;
+}
+
+int wg_ascii_format_size(const double* values, int64_t count, uint64_t* nbytes, void* scratch, void* stream) {
+  if (count < 0 || !nbytes || !scratch || (count > 0 && !values)) return wg::set_error(WG_EARG, "null buffer");
+  cudaStream_t st = wg::as_stream(stream);
+  if (count == 0) {
+    WG_CUDA_TRY(cudaMemsetAsync(nbytes, 0, sizeof(uint64_t), st));
+    return WG_OK;
+  }
+  const int64_t blocks = (count + kFmtThreads - 1) / kFmtThreads;
+  if (blocks > 0x7fffffff) return wg::set_error(WG_ELIMIT, "too many values");
+  unsigned long long* bb = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(scratch) + 256);
+  fmt_len_kernel<<<(unsigned)blocks, kFmtThreads, 0, st>>>(values, count, bb);
+  WG_LAUNCH_CHECK("fmt_len_kernel");
+  scan_kernel<<<1, 1024, 0, st>>>(bb, blocks, reinterpret_cast<unsigned long long*>(nbytes));
+  WG_LAUNCH_CHECK("scan_kernel");
+  return WG_OK;
+}
+
+int wg_ascii_format_write(const double* values, int64_t count, int64_t cols, uint8_t* out, void* scratch,
+                          void* stream) {
+  if (count < 0 || cols < 1 || !scratch || (count > 0 && (!values || !out))) return wg::set_error(WG_EARG, "bad args");
+  if (count == 0) return WG_OK;
+  const int64_t blocks = (count + kFmtThreads - 1) / kFmtThreads;
+  const unsigned long long* bb = reinterpret_cast<const unsigned long long*>(static_cast<unsigned char*>(scratch) + 256);
+  fmt_write_kernel<<<(unsigned)blocks, kFmtThreads, 0, wg::as_stream(stream)>>>(values, count, cols, bb, out);
+  WG_LAUNCH_CHECK("fmt_write_kernel");
+  return WG_OK;
+}
+
+}  // extern "C"
