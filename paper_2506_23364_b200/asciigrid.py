@@ -64,9 +64,11 @@ def format_number(v: float) -> str:
     return repr(f)
 
 
-def _as_bytes(text) -> bytes:
-    if isinstance(text, (bytes, bytearray, memoryview)):
-        return bytes(text) if not isinstance(text, bytes) else text
+def _as_bytes(text):
+    if isinstance(text, (bytes, bytearray)):
+        return text
+    if isinstance(text, memoryview):
+        return text if text.contiguous and text.format in ("B", "b", "c") else text.tobytes()
     if not text.isascii():
         raise AsciiGridError("document is not ASCII")
     return text.encode("ascii")
@@ -139,7 +141,19 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
     """Parse an ASCII grid document into a device-resident DemGrid
     (asciigrid.py:42-143)."""
     data = _as_bytes(text)
-    header, body_off, _ = _header(data)
+    if isinstance(data, memoryview):
+        head = bytes(data[: 1 << 16])
+        try:
+            header, body_off, lines = _header(head)
+        except AsciiGridError:
+            header = None
+        if header is None or (len(lines) == 6 and body_off == len(head) < len(data)):
+            head = bytes(data)  # a header longer than 64 KiB: read it from the whole document
+            header, body_off, _ = _header(head)
+        full = lambda: bytes(data)  # noqa: E731  (error paths only)
+    else:
+        header, body_off, _ = _header(data)
+        full = lambda: data  # noqa: E731
     ncols, nrows = int(header["ncols"]), int(header["nrows"])
     expected = ncols * nrows
     L = _lib.lib()
@@ -156,9 +170,10 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
         raise AsciiGridError("document is not ASCII")
     if found != expected:
         if found < expected:
-            raise AsciiGridError(f"expected {expected} elevation values, found {found}", line=_count_lines(data))
+            raise AsciiGridError(f"expected {expected} elevation values, found {found}",
+                                 line=_count_lines(full()))
         off = int(_device.read_small(starts[expected:expected + 1])[0])
-        line, col = _line_col(data, off)
+        line, col = _line_col(full(), off)
         raise AsciiGridError(f"expected {expected} elevation values, found {found}", line=line, column=col)
     values = torch.empty(expected, dtype=torch.float64, device=dev)
     bad = torch.empty(1, dtype=torch.int64, device=dev)
@@ -167,6 +182,7 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
     first_bad = int(_device.read_small(bad)[0]) & _NO_BAD
     if first_bad != _NO_BAD:
         off = int(_device.read_small(starts[first_bad:first_bad + 1])[0])
+        data = full()
         end = off
         while end < n and data[end:end + 1] not in (b" ", b"\t", b"\n", b"\x0b", b"\x0c", b"\r", b"\x1c", b"\x1d",
                                                    b"\x1e", b"\x1f"):
@@ -182,8 +198,10 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
         raise AsciiGridError(str(exc)) from exc
 
 
-def write_ascii_grid_bytes(grid: DemGrid) -> bytes:
-    """The canonical ASCII grid document as bytes (body formatted on the GPU)."""
+def write_ascii_grid_bytes(grid: DemGrid) -> memoryview:
+    """The canonical ASCII grid document as a bytes-like buffer (body
+    formatted on the GPU); write it to a file or pass it to
+    ``parse_ascii_grid`` without a copy."""
     header_values = (grid.ncols, grid.nrows, grid.origin_x, grid.origin_y, grid.cellsize, grid.nodata)
     head = "".join(f"{key} {format_number(val)}\n" for key, val in zip(_CANONICAL_KEYS, header_values)).encode()
     L = _lib.lib()
@@ -197,15 +215,20 @@ def write_ascii_grid_bytes(grid: DemGrid) -> bytes:
     out[: len(head)].copy_(torch.tensor(list(head), dtype=torch.uint8))
     _lib.check(L.wg_ascii_format_write(_lib.ptr(v), count, grid.ncols, _lib.ptr(out[len(head):]), _lib.ptr(scratch),
                                        _lib.stream_ptr()))
-    host = torch.empty(out.shape, dtype=torch.uint8, pin_memory=True)
-    host.copy_(out)
-    return host.numpy().tobytes()
+    # one pageable D2H straight into uninitialised host memory: at multi-GB
+    # sizes first-touch page zeroing (~5 GB/s) bounds any strategy, and
+    # bytearray's zero-fill or pinned staging only add to it
+    # (tools/d2h_probe.py)
+    buf = np.empty(out.numel(), dtype=np.uint8)
+    if buf.size:
+        torch.from_numpy(buf).copy_(out)
+    return memoryview(buf)
 
 
 def write_ascii_grid(grid: DemGrid) -> str:
     """Serialize a DemGrid to the canonical ASCII grid text
     (asciigrid.py:146-157)."""
-    return write_ascii_grid_bytes(grid).decode("ascii")
+    return str(write_ascii_grid_bytes(grid), "ascii")
 
 
 def read_ascii_grid(path) -> DemGrid:

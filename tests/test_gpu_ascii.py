@@ -161,3 +161,18 @@ def test_random_tokens_parse_like_cpython(ag):
         want = np.array(toks, dtype=np.float64)
     got = np.asarray(ag.parse_ascii_grid(doc).elevations).ravel()
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+def test_bytes_buffer_round_trip(ag):
+    """write_ascii_grid_bytes -> parse_ascii_grid without a str in between."""
+    from paper_2506_23364_b200 import gen_parabola
+
+    grid, _ = gen_parabola()
+    buf = ag.write_ascii_grid_bytes(grid)
+    assert hashlib.sha256(buf).hexdigest() == GOLDEN["parabola"]["sha"]
+    g = ag.parse_ascii_grid(buf)
+    assert sha(np.ascontiguousarray(g.elevations).tobytes()) == GOLDEN["parabola"]["elev_sha"]
+    with pytest.raises(ag.AsciiGridError, match="invalid elevation value"):
+        raw = bytes(buf)
+        i = raw.rindex(b" ")
+        ag.parse_ascii_grid(memoryview(raw[:i] + b" x" + raw[i + 1:]))

@@ -2,6 +2,7 @@
 fixtures (tests/golden/make_golden.py).  No GPU."""
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -103,3 +104,26 @@ def test_npref_parabola_pyramid_hashes(parabola_host, golden_meta):
     z, _ = traj.run_avalanche(elev, ox, oy, cs, mask)
     levels = npref.mipmap(npref.colorize(z, DEFAULT_RUNOUT_COLORMAP.stops))
     assert [sha(lv) for lv in levels] == golden_meta["parabola"]["default"]["levels_sha"]
+
+
+def test_ascii_oracle_matches_reference_fixtures():
+    """oracle/asciigrid_ref.py (the CPU baseline of tools/bench_ascii.py)
+    reproduces the reference-run ASCII fixtures."""
+    import hashlib
+    import json
+
+    from oracle import asciigrid_ref
+
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "ascii_golden.json").read_text())
+    for case in g["write"]:
+        z = np.array([float.fromhex(h) for h in case["values_hex"]]).reshape(case["nrows"], case["ncols"])
+        hdr = (case["ncols"], case["nrows"], case["origin_x"], case["origin_y"], case["cellsize"], case["nodata"])
+        text = asciigrid_ref.write_text(hdr, z)
+        assert hashlib.sha256(text.encode()).hexdigest() == case["sha"]
+        back = asciigrid_ref.parse_body(text, case["nrows"], case["ncols"])
+        assert np.array_equal(back, z)
+    for case in g["parse"]:
+        if "ok" in case and case["ok"]["values_hex"] is not None:
+            ok = case["ok"]
+            v = asciigrid_ref.parse_body(case["doc"], ok["nrows"], ok["ncols"])
+            assert hashlib.sha256(v.tobytes()).hexdigest() == ok["sha"]
