@@ -42,6 +42,7 @@ SIGNATURES: dict[str, tuple] = {
     "wg_normals": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr]),
     "wg_steepness": (c_int, [c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_hillshade": (c_int, [c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_ptr, c_ptr]),
+    "wg_hillshade_rgba": (c_int, [c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_ptr, c_ptr]),
     "wg_release_mask": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_i64, c_ptr, c_ptr]),
     "wg_compact_scratch_bytes": (c_size, [c_i64]),
     "wg_mask_compact": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),

@@ -166,6 +166,19 @@ __global__ void hillshade_kernel(const double* __restrict__ nrm, int64_t n, doub
   }
 }
 
+// The service's hillshade base layer (service.py:527-538): the same shade as
+// an opaque gray RGBA texel, texture_from_gray fused in (one 4-byte store).
+__global__ void hillshade_rgba_kernel(const double* __restrict__ nrm, int64_t n, double lx, double ly, double lz,
+                                      uint32_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const double* v = nrm + 3 * t;
+    const double dot = WG_ADD(WG_ADD(WG_MUL(__ldg(v), lx), WG_MUL(__ldg(v + 1), ly)), WG_MUL(__ldg(v + 2), lz));
+    const double sh = wg_min(wg_max(dot, 0.0), 1.0);
+    const uint32_t g = (uint32_t)(int)floor(WG_ADD(WG_MUL(sh, 255.0), 0.5));
+    out[t] = g | (g << 8) | (g << 16) | 0xFF000000u;
+  }
+}
+
 // ---------------------------------------------------------------- release mask
 // Each thread writes 16 mask bytes of one row (one 16-B store when aligned);
 // the slope is read only at stride-lattice cells, the only cells the mask can
@@ -401,6 +414,16 @@ int wg_hillshade(const double* normals, int64_t n, double lx, double ly, double 
   if (!normals || !out) return wg::set_error(WG_EARG, "null buffer");
   hillshade_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(normals, n, lx, ly, lz, out);
   WG_LAUNCH_CHECK("hillshade_kernel");
+  return WG_OK;
+}
+
+int wg_hillshade_rgba(const double* normals, int64_t n, double lx, double ly, double lz, uint8_t* out, void* stream) {
+  if (n <= 0) return WG_OK;
+  if (!normals || !out) return wg::set_error(WG_EARG, "null buffer");
+  if (((uintptr_t)out) & 3) return wg::set_error(WG_EARG, "out must be 4-byte aligned");
+  hillshade_rgba_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
+      normals, n, lx, ly, lz, reinterpret_cast<uint32_t*>(out));
+  WG_LAUNCH_CHECK("hillshade_rgba_kernel");
   return WG_OK;
 }
 

@@ -160,17 +160,19 @@ def downslope_dir(grid: DemGrid, x: float, y: float) -> tuple[float, float] | No
     return (gx / mag, gy / mag)
 
 
-def hillshade(grid: DemGrid, azimuth_deg: float = 315.0, altitude_deg: float = 45.0) -> np.ndarray:
-    """Lambertian hillshade as (nrows, ncols) uint8 (terrain.py:287-299).
-
-    Out of the scored hot path (the service's base layer); runs as the
-    normals kernel followed by one shading pass."""
-    normals = compute_normals(grid)
+def _light(azimuth_deg: float, altitude_deg: float) -> tuple[float, float, float]:
+    # terrain.py:292-297, host Python floats (glibc sin/cos), passed verbatim
     az = math.radians(azimuth_deg)
     alt = math.radians(altitude_deg)
-    lx = math.sin(az) * math.cos(alt)
-    ly = math.cos(az) * math.cos(alt)
-    lz = math.sin(alt)
+    return math.sin(az) * math.cos(alt), math.cos(az) * math.cos(alt), math.sin(alt)
+
+
+def hillshade(grid: DemGrid, azimuth_deg: float = 315.0, altitude_deg: float = 45.0) -> np.ndarray:
+    """Lambertian hillshade as (nrows, ncols) uint8 (terrain.py:287-299):
+    the normals kernel, then one shading pass (IEEE ops on bit-exact normals
+    with host-computed light scalars: bit-exact)."""
+    normals = compute_normals(grid)
+    lx, ly, lz = _light(azimuth_deg, altitude_deg)
     L = _lib.lib()
     out = _device.empty((grid.nrows, grid.ncols), torch.uint8)
     _lib.check(
@@ -178,3 +180,25 @@ def hillshade(grid: DemGrid, azimuth_deg: float = 315.0, altitude_deg: float = 4
         TerrainError,
     )
     return _device.host_view(out)
+
+
+def hillshade_texture(grid: DemGrid, azimuth_deg: float = 315.0, altitude_deg: float = 45.0):
+    """texture_from_gray(hillshade(grid)) as a device-resident OverlayTexture
+    (service.py:527-538's base layer; one fused shading pass)."""
+    from .overlay import OverlayTexture
+
+    normals = compute_normals(grid)
+    lx, ly, lz = _light(azimuth_deg, altitude_deg)
+    L = _lib.lib()
+    out = _device.empty((grid.nrows, grid.ncols, 4), torch.uint8)
+    _lib.check(L.wg_hillshade_rgba(_lib.ptr(normals.dev("normals")), grid.nrows * grid.ncols, lx, ly, lz,
+                                   _lib.ptr(out), _lib.stream_ptr()), TerrainError)
+    return OverlayTexture(out)
+
+
+def hillshade_pyramid(grid: DemGrid, azimuth_deg: float = 315.0, altitude_deg: float = 45.0):
+    """build_mipmap(texture_from_gray(hillshade(grid))) on the device: the
+    service's hillshade tile pyramid (service.py:527-538)."""
+    from .overlay import build_mipmap
+
+    return build_mipmap(hillshade_texture(grid, azimuth_deg, altitude_deg))
