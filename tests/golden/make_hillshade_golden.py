@@ -1,4 +1,5 @@
-"""Golden fixtures for the hillshade base layer, made
+"""Golden fixtures for the hillshade base layer and its
+served tiles (extract_tile, §8f row 2), made
 by running the REFERENCE (terrain.py:287-299 hillshade; service.py:527-538
 build_mipmap(texture_from_gray(gray))) in this container:
 tests/golden/hillshade_golden.json.  Inputs: the bundled parabola and the
@@ -27,7 +28,7 @@ def main() -> None:
     sys.path.insert(0, str(REF))
     from demflow import gen_parabola
     from demflow.grid import DemGrid
-    from demflow.overlay import build_mipmap, texture_from_gray
+    from demflow.overlay import build_mipmap, extract_tile, max_tile_zoom, texture_from_gray
     from demflow.terrain import hillshade
 
     meta = json.loads((HERE / "golden_meta.json").read_text())
@@ -44,8 +45,18 @@ def main() -> None:
         for az, alt in ((315.0, 45.0), (90.0, 30.0), (200.0, 70.0)):
             gray = hillshade(g, az, alt)
             pyr = build_mipmap(texture_from_gray(gray))
-            cases.append({"grid": name, "array": key, "azimuth": az, "altitude": alt, "gray_sha": sha(gray),
-                          "levels_sha": [sha(lv.pixels) for lv in pyr.levels]})
+            case = {"grid": name, "array": key, "azimuth": az, "altitude": alt, "gray_sha": sha(gray),
+                    "levels_sha": [sha(lv.pixels) for lv in pyr.levels]}
+            if az == 315.0:  # the service's tiles of this base layer (extract_tile, overlay.py:231-252)
+                tiles = {}
+                for tile_px in (256, 64):
+                    zmax = max_tile_zoom(pyr.width, pyr.height, tile_px)
+                    for z in range(zmax + 1):
+                        for ty in range(1 << z):
+                            for tx in range(1 << z):
+                                tiles[f"{tile_px}/{z}/{tx}/{ty}"] = sha(extract_tile(pyr, z, tx, ty, tile_px).pixels)
+                case["tiles_sha"] = tiles
+            cases.append(case)
     (HERE / "hillshade_golden.json").write_text(json.dumps({"reference": str(REF), "cases": cases}, indent=1) + "\n")
     print(f"wrote {len(cases)} cases")
 
