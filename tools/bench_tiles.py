@@ -1,0 +1,118 @@
+"""Measurement of the tile-serving row: every 256-px
+tile of every zoom of two 8192^2 pyramids -- the hillshade base layer of
+synth_dem(8192, 1) and the avalanche runout overlay of the stock graph at
+C4 -- extracted and PNG-encoded on the GPU in one launch per zoom; kernel
+time (CUDA events) and end to end (PNG bytes on the host).  Beside it, the
+reference path (numpy slice + Pillow PNG, overlay.py:231-260) on the host
+over a sample of the same tiles.  Prints one JSON line."""
+
+import argparse
+import io
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2506_23364_b200 as wf  # noqa: E402
+from paper_2506_23364_b200 import _device, _lib  # noqa: E402
+from paper_2506_23364_b200.synth import synth_dem_device  # noqa: E402
+from paper_2506_23364_b200.terrain import hillshade_pyramid  # noqa: E402
+
+
+def all_tiles(pyr, tile_px=256):
+    zmax = wf.max_tile_zoom(pyr.width, pyr.height, tile_px)
+    return zmax, [(z, tx, ty) for z in range(zmax + 1) for ty in range(1 << z) for tx in range(1 << z)]
+
+
+def gpu_encode(pyr, L, tile_px=256):
+    """(kernel ms, e2e ms, total bytes, n tiles) for all tiles of all zooms."""
+    zmax, tiles = all_tiles(pyr, tile_px)
+    cap = int(L.wg_png_capacity(tile_px, tile_px))
+    per_zoom = {}
+    for z, tx, ty in tiles:
+        per_zoom.setdefault(z, []).append((tx, ty))
+    # kernels only
+    bufs = {}
+    for z, t in per_zoom.items():
+        txy = torch.tensor([v for p in t for v in p], dtype=torch.int32, device="cuda")
+        bufs[z] = (txy, _device.empty((cap * len(t),), torch.uint8), _device.empty((len(t),), torch.int64))
+    best = 1e30
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for z, t in per_zoom.items():
+            level = pyr.levels[zmax - z].dev("pixels")
+            txy, out, lens = bufs[z]
+            L.wg_png_tiles(_lib.ptr(level), int(level.shape[1]), int(level.shape[0]), tile_px, _lib.ptr(txy), len(t),
+                           _lib.ptr(out), cap, _lib.ptr(lens), _lib.stream_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    total = sum(int(b[2].sum()) for b in bufs.values())
+    del bufs
+    # end to end through the public API (bytes on the host)
+    t0 = time.perf_counter()
+    n = 0
+    nbytes = 0
+    for z in range(zmax + 1):
+        pngs = wf.tile_pngs(pyr, z)
+        n += len(pngs)
+        nbytes += sum(len(v) for v in pngs.values())
+    e2e = (time.perf_counter() - t0) * 1e3
+    return best, e2e, nbytes, n, total
+
+
+def cpu_encode(pyr, sample, tile_px=256):
+    """The reference path on the host for a sample of tiles: (s, bytes)."""
+    from PIL import Image
+
+    zmax, tiles = all_tiles(pyr, tile_px)
+    levels = {z: np.asarray(pyr.levels[zmax - z].pixels) for z in range(zmax + 1)}
+    pick = tiles[:: max(1, len(tiles) // sample)]
+    t0 = time.perf_counter()
+    nb = 0
+    for z, tx, ty in pick:
+        src = levels[z][ty * tile_px : (ty + 1) * tile_px, tx * tile_px : (tx + 1) * tile_px]
+        canvas = np.zeros((tile_px, tile_px, 4), dtype=np.uint8)
+        canvas[: src.shape[0], : src.shape[1]] = src
+        buf = io.BytesIO()
+        Image.fromarray(canvas, mode="RGBA").save(buf, format="PNG")
+        nb += len(buf.getvalue())
+    return time.perf_counter() - t0, nb, len(pick)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sample", type=int, default=200)
+    a = ap.parse_args()
+    _lib.build()
+    L = _lib.lib()
+    n = 8192
+    dem = wf.DemGrid(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
+    hs = hillshade_pyramid(dem)
+    g = wf.build_avalanche_graph(dem.extent, wf.AvalancheParams(particles_per_release_cell=256, seed=0),
+                                 wf.SteepnessRelease(30.0, 45.0, stride=16), zoom=2)
+    g.bind("world", dem)
+    ov = wf.Executor().execute(g).value("avalanche_overlay", "overlay")
+    out = {"metric": "PNG tiles/s", "unit": "tiles/s", "config": {
+        "workload": "all 256-px tiles, zooms 0-5 (1365 per pyramid) of two 8192^2 pyramids: hillshade of "
+                    "synth_dem(8192, 1) and the stock avalanche overlay (stride 16, 256 particles/cell)"}}
+    for name, pyr in (("hillshade", hs), ("overlay", ov)):
+        k_ms, e2e_ms, nbytes, ntiles, _ = gpu_encode(pyr, L)
+        cpu_s, cpu_bytes, cpu_n = cpu_encode(pyr, a.sample)
+        out[name] = {"tiles": ntiles, "kernel_ms": k_ms, "value": ntiles / (k_ms / 1e3), "e2e_ms": e2e_ms,
+                     "e2e_value": ntiles / (e2e_ms / 1e3), "mean_png_bytes": nbytes / ntiles,
+                     "cpu_baseline": {"kind": "reference path (numpy slice + Pillow PNG)", "cores": 1,
+                                      "sample": f"{cpu_n} evenly spaced tiles of the same pyramid",
+                                      "value": cpu_n / cpu_s, "unit": "tiles/s",
+                                      "mean_png_bytes": cpu_bytes / cpu_n}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
