@@ -77,8 +77,9 @@ SIGNATURES: dict[str, tuple] = {
     "wg_synth_combine": (c_int, [c_ptr, c_ptr, c_ptr, c_int, c_i64, c_i64, c_ptr, c_ptr]),
     "wg_sub_scalar": (c_int, [c_ptr, c_i64, c_dbl, c_ptr]),
     "wg_png_capacity": (c_i64, [c_i64, c_i64]),
-    "wg_png_tiles": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
-    "wg_png_encode": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
+    "wg_png_scratch_bytes": (c_size, [c_i64, c_i64, c_i64]),
+    "wg_png_tiles": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
+    "wg_png_encode": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_ascii_tokenize_scratch_bytes": (c_size, [c_i64]),
     "wg_ascii_tokenize": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_ascii_parse": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),

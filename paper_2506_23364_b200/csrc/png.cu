@@ -1,22 +1,36 @@
 // Tile serving on the device: extract_tile + encode_png
 // (/root/reference/pkg/src/demflow/overlay.py:221-260; service.py:351-360).
 //
-// One CTA per tile reads its tile_px x tile_px window of a pyramid level
-// (texels outside the level are transparent black, overlay.py:247-251) and
-// writes a complete PNG file: signature, IHDR (8-bit RGBA, non-interlaced),
+// Each image (a tile_px x tile_px tile of a pyramid level -- texels outside
+// the level are transparent black, overlay.py:247-251 -- or a whole texture)
+// becomes a complete PNG file: signature, IHDR (8-bit RGBA, non-interlaced),
 // one IDAT holding a zlib stream, IEND.  The reference encodes with Pillow
 // (zlib deflate); its byte stream is not pinned, so parity is the decoded
 // image (decode_png(encode_png(t)) == t) and the stream's own checksums.
 //
-// Encoding: per scanline, warp-parallel, the PNG filter (None/Sub/Up/Avg/
-// Paeth) with the least sum of |signed residual| (libpng's heuristic); the
-// residual bytes are deflated as ONE fixed-Huffman block whose matches are
-// byte runs (distance 1) -- transparent and flat areas become runs of zeros
-// under Sub/Up.  Each lane tokenises its 32-byte slice; pass A sums bits per
-// row, a block scan places the rows, pass B writes every token's bits with
-// 32-bit atomic ORs into the zeroed stream.  Adler-32 of the filtered data
-// comes from per-lane position-weighted sums; CRC-32 of the IDAT chunk from
-// per-lane CRCs joined with crc32_combine's GF(2) shift (zlib's method).
+// Three kernels over a batch of images:
+//   filter_kernel  one CTA per image, warp per row: the PNG filter (None/Sub/
+//                  Up/Avg/Paeth) with the least sum of |signed residual|
+//                  (libpng's heuristic); writes the filtered stream (filter
+//                  byte + residuals per row) and its Adler-32;
+//   lz_kernel      one warp per ~32 KiB chunk of rows: greedy LZ77 parse
+//                  with a 32-position lookahead (lane k measures position
+//                  i + k; the first match ends the step).
+//                  Candidates per position: the 4 most recent positions with
+//                  the same 3-byte hash (a per-chunk bucket table in global
+//                  memory, inserted warp-parallel, one writer per bucket and
+//                  token so the parse is deterministic) and the image-shaped
+//                  distances 1, 4, row, 2 rows, row +- 4; each lane measures
+//                  one candidate, the warp keeps the longest (ties: the
+//                  lowest lane); matches may reach back 32 KiB into earlier
+//                  chunks.  Tokens go to a per-chunk array;
+//   emit_kernel    one CTA per image: symbol histograms, dynamic Huffman
+//                  codes (Moffat-Katajainen lengths limited to 15 bits,
+//                  canonical codes, run-length coded code lengths; one
+//                  thread), the tokens' bit lengths, a block scan, 32-bit
+//                  atomic ORs into the zeroed stream, then zlib/Adler, the
+//                  IDAT CRC-32 (per-lane CRCs joined by crc32_combine's GF(2)
+//                  shift) and IEND.
 #include "wg_internal.cuh"
 
 namespace {
@@ -58,36 +72,6 @@ __device__ __forceinline__ void lit_code(unsigned lit, uint32_t& code, int& len)
   }
 }
 
-// length L (3..258) + distance 1: length code with extra bits, then the
-// 5-bit distance code 0
-__device__ __forceinline__ void match_code(unsigned L, uint32_t& code, int& len) {
-  unsigned sym, extra = 0, ebits = 0;
-  if (L == 258) {
-    sym = 285;
-  } else if (L <= 10) {
-    sym = 254 + L;
-  } else {
-    // codes 265..284: 4 codes per extra-bit count, base lengths 11,13,..
-    const unsigned l = L - 3;  // 8..254
-    const int eb = 31 - __clz(l) - 2;  // extra bits (1..5)
-    const unsigned grp = (l >> eb) - 4;  // 0..3 within the group
-    sym = 265 + (eb - 1) * 4 + grp;
-    extra = l & ((1u << eb) - 1);
-    ebits = eb;
-  }
-  uint32_t c;
-  int n;
-  if (sym < 280) {
-    c = rev(sym - 256, 7);
-    n = 7;
-  } else {
-    c = rev(0xC0 + (sym - 280), 8);
-    n = 8;
-  }
-  code = c | (extra << n);  // extra bits follow, LSB first
-  len = n + (int)ebits + 5;  // + distance code 0 (five zero bits)
-}
-
 // Bit sink: count (kWrite false) or OR into the zeroed stream at bit offset.
 template <bool kWrite>
 struct Bits {
@@ -104,38 +88,6 @@ struct Bits {
     pos += (uint64_t)len;
   }
 };
-
-// Tokenise one lane's residual bytes (runs -> distance-1 matches).
-template <bool kWrite>
-__device__ void emit_bytes(Bits<kWrite>& out, const uint32_t* f, int nbytes, unsigned prev, bool has_prev) {
-  int i = 0;
-  while (i < nbytes) {
-    const unsigned b = (f[i >> 2] >> (8 * (i & 3))) & 255u;
-    int j = i + 1;
-    while (j < nbytes && ((f[j >> 2] >> (8 * (j & 3))) & 255u) == b) j++;
-    int avail = j - i;
-    uint32_t code;
-    int len;
-    if (!(has_prev && prev == b)) {
-      lit_code(b, code, len);
-      out.put(code, len);
-      avail -= 1;
-    }
-    while (avail >= 3) {
-      const int L = avail > 258 ? 258 : avail;
-      match_code((unsigned)L, code, len);
-      out.put(code, len);
-      avail -= L;
-    }
-    for (; avail > 0; avail--) {
-      lit_code(b, code, len);
-      out.put(code, len);
-    }
-    prev = b;
-    has_prev = true;
-    i = j;
-  }
-}
 
 // One PNG image: W x H texels read from a level at (x0, y0); texels outside
 // the level are transparent black (the tile canvas, overlay.py:247-251).
@@ -215,61 +167,6 @@ __device__ __forceinline__ int residuals(const Img& g, int r, int c0, int ftype,
   return n < 0 ? 0 : (n > kLanePx ? kLanePx : n);
 }
 
-// Visit row r: the filter byte then every chunk's lane slices, chaining the
-// previous byte across lanes and chunks.  kWrite false: returns the row's
-// bits (lane 0 holds them) and accumulates the Adler sums; kWrite true:
-// writes the bits starting at row_bit.
-template <bool kWrite>
-__device__ uint64_t visit_row(const Img& g, int r, uint32_t* words, uint64_t row_bit, unsigned long long& sumA,
-                              unsigned long long& sumW) {
-  const int lane = threadIdx.x & 31;
-  const int ftype = choose_filter(g, r);
-  uint32_t code;
-  int len;
-  lit_code((unsigned)ftype, code, len);
-  if (kWrite && lane == 0) {
-    Bits<true> o{words, row_bit};
-    o.put(code, len);
-  }
-  const int64_t row_base = (int64_t)r * (4 * (int64_t)g.W + 1);
-  if (!kWrite && lane == 0) {
-    sumA += (unsigned)ftype;
-    sumW += (unsigned long long)row_base * (unsigned)ftype;
-  }
-  uint64_t bits = (uint64_t)len;  // warp-uniform running total
-  unsigned carry = (unsigned)ftype;  // byte before the chunk
-  for (int cbase = 0; cbase < g.W; cbase += kChunkPx) {
-    const int c0 = cbase + lane * kLanePx;
-    uint32_t f[kLanePx];
-    const int n = residuals(g, r, c0, ftype, f);
-    const unsigned last = (f[(n > 0 ? n : 1) - 1] >> 24) & 255u;
-    unsigned prev = __shfl_up_sync(0xffffffffu, last, 1);
-    if (lane == 0) prev = carry;
-    Bits<false> cnt{nullptr, 0};
-    if (n > 0) emit_bytes(cnt, f, 4 * n, prev, true);
-    uint64_t x = cnt.pos;  // inclusive scan of lane bits
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (kWrite && n > 0) {
-      Bits<true> o{words, row_bit + bits + x - cnt.pos};
-      emit_bytes(o, f, 4 * n, prev, true);
-    }
-    if (!kWrite) {
-      for (int k = 0; k < 4 * n; k++) {
-        const unsigned b = (f[k >> 2] >> (8 * (k & 3))) & 255u;
-        sumA += b;
-        sumW += (unsigned long long)(row_base + 1 + 4 * (int64_t)c0 + k) * b;
-      }
-    }
-    bits += __shfl_sync(0xffffffffu, x, 31);
-    const int m = min(32, (g.W - cbase + kLanePx - 1) / kLanePx);  // lanes with texels
-    carry = __shfl_sync(0xffffffffu, last, m - 1);
-  }
-  return bits;
-}
-
 __device__ uint32_t crc_table_entry(uint32_t n) {
   uint32_t c = n;
   for (int k = 0; k < 8; k++) c = (c & 1) ? kCrcPoly ^ (c >> 1) : c >> 1;
@@ -332,69 +229,629 @@ __device__ uint32_t warp_crc32(const uint8_t* p, int64_t n, const uint32_t* tabl
   return __shfl_sync(0xffffffffu, crc, 0);
 }
 
-// One CTA per image.  txy: image origins in tile units of T (tiles), or
-// null for one W x H image at (0, 0) (encode_png of a whole texture).
-__global__ void __launch_bounds__(kPngThreads) png_kernel(const uint8_t* __restrict__ level, int64_t lw, int64_t lh,
-                                                          int W, int H, const int32_t* __restrict__ txy,
-                                                          uint8_t* __restrict__ out, int64_t cap,
-                                                          int64_t* __restrict__ lens) {
-  extern __shared__ uint64_t s_rows[];  // H row bit counts, then offsets
-  __shared__ uint32_t s_table[256];
-  __shared__ unsigned long long s_adA, s_adB;
-  __shared__ uint64_t s_total;
+
+// fixed-Huffman length symbol for L (3..258): reversed code | extra << n, bits
+__device__ __forceinline__ void len_code(unsigned L, uint32_t& code, int& len) {
+  unsigned sym, extra = 0, ebits = 0;
+  if (L == 258) {
+    sym = 285;
+  } else if (L <= 10) {
+    sym = 254 + L;
+  } else {
+    const unsigned l = L - 3;  // 8..254
+    const int eb = 31 - __clz(l) - 2;  // extra bits (1..5)
+    sym = 265 + (eb - 1) * 4 + ((l >> eb) - 4);
+    extra = l & ((1u << eb) - 1);
+    ebits = eb;
+  }
+  int n;
+  uint32_t c;
+  if (sym < 280) {
+    c = rev(sym - 256, 7);
+    n = 7;
+  } else {
+    c = rev(0xC0 + (sym - 280), 8);
+    n = 8;
+  }
+  code = c | (extra << n);
+  len = n + (int)ebits;
+}
+
+// fixed distance code (5 bits, reversed) + extra bits for d in 1..32768
+__device__ __forceinline__ void dist_code(unsigned d, uint32_t& code, int& len) {
+  unsigned sym, extra = 0;
+  int eb = 0;
+  if (d <= 4) {
+    sym = d - 1;
+  } else {
+    const unsigned l = d - 1;
+    eb = 31 - __clz(l) - 1;
+    sym = 2 * (eb + 1) + ((l >> eb) & 1);
+    extra = l & ((1u << eb) - 1);
+  }
+  code = rev(sym, 5) | (extra << 5);
+  len = 5 + eb;
+}
+
+// token: literal byte b (< 256), or match (L << 16) | (d - 1) with L >= 3
+__device__ __forceinline__ int token_bits(uint32_t t) {
+  if (t < 256) return t < 144 ? 8 : 9;
+  uint32_t c;
+  int a, b;
+  len_code(t >> 16, c, a);
+  dist_code((t & 0xFFFF) + 1, c, b);
+  return a + b;
+}
+
+template <bool kWrite>
+__device__ __forceinline__ void put_token(Bits<kWrite>& o, uint32_t t) {
+  uint32_t c;
+  int n;
+  if (t < 256) {
+    lit_code(t, c, n);
+    o.put(c, n);
+  } else {
+    len_code(t >> 16, c, n);
+    o.put(c, n);
+    dist_code((t & 0xFFFF) + 1, c, n);
+    o.put(c, n);
+  }
+}
+
+// Per-image scratch layout (wg_png_scratch_bytes).
+struct Layout {
+  int64_t nbytes;    // filtered stream bytes: (4W + 1) * H
+  int rows_per_chunk, nchunks;
+  int64_t f_off, tok_off, tab_off, meta_off, per_image;
+};
+
+constexpr int kBuckets = 1024;  // per chunk, 4 slots each
+constexpr int kSlots = 4;
+constexpr int kWindow = 32768;
+
+__host__ __device__ inline Layout layout_of(int64_t W, int64_t H) {
+  Layout l;
+  l.nbytes = (4 * W + 1) * H;
+  const int64_t row = 4 * W + 1;
+  l.rows_per_chunk = (int)(row >= kWindow ? 1 : kWindow / row);
+  l.nchunks = (int)((H + l.rows_per_chunk - 1) / l.rows_per_chunk);
+  auto up = [](int64_t v) { return (v + 255) / 256 * 256; };
+  l.f_off = 0;
+  l.tok_off = up(l.nbytes + 8);  // + slack for 4-byte compares
+  l.tab_off = l.tok_off + up(l.nbytes * 4);
+  l.meta_off = l.tab_off + up((int64_t)l.nchunks * kBuckets * kSlots * 4);
+  l.per_image = l.meta_off + up(8 + (int64_t)l.nchunks * 4);  // adler (u32) + pad + token counts
+  return l;
+}
+
+struct Batch {
+  const uint8_t* level;
+  int64_t lw, lh;
+  int W, H;
+  const int32_t* txy;  // tile coords (units of W/H) or null
+  uint8_t* scratch;
+  Layout lay;
+  uint8_t* out;
+  int64_t cap;
+  int64_t* lens;
+};
+
+__device__ __forceinline__ Img img_of(const Batch& b, int i) {
+  return Img{b.level, b.lw, b.lh, b.txy ? (int64_t)b.txy[2 * i] * b.W : 0, b.txy ? (int64_t)b.txy[2 * i + 1] * b.H : 0,
+             b.W, b.H};
+}
+
+// ---- kernel 1: filtered stream + Adler-32 ----------------------------------
+__global__ void __launch_bounds__(kPngThreads) filter_kernel(Batch b) {
+  __shared__ unsigned long long s_a, s_w;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = kPngThreads / 32;
-  Img g{level, lw, lh, txy ? (int64_t)txy[2 * blockIdx.x] * W : 0, txy ? (int64_t)txy[2 * blockIdx.x + 1] * H : 0,
-        W, H};
-  uint8_t* img = out + (int64_t)blockIdx.x * cap;
-  const int64_t nbytes = (4 * (int64_t)W + 1) * H;  // filtered data (zlib payload)
-  for (int i = threadIdx.x; i < 256; i += kPngThreads) s_table[i] = crc_table_entry((uint32_t)i);
-  if (threadIdx.x == 0) s_adA = s_adB = 0;
+  const Img g = img_of(b, blockIdx.x);
+  uint8_t* base = b.scratch + (int64_t)blockIdx.x * b.lay.per_image;
+  uint8_t* F = base + b.lay.f_off;
+  if (threadIdx.x == 0) s_a = s_w = 0;
   __syncthreads();
-  // ---- pass A: bits per row, Adler sums
   unsigned long long sumA = 0, sumW = 0;
-  for (int r = warp; r < H; r += nw) {
-    const uint64_t bits = visit_row<false>(g, r, nullptr, 0, sumA, sumW);
-    if (lane == 0) s_rows[r] = bits;
+  const int64_t row = 4 * (int64_t)g.W + 1;
+  for (int r = warp; r < g.H; r += kPngThreads / 32) {
+    const int ftype = choose_filter(g, r);
+    const int64_t rb = (int64_t)r * row;
+    if (lane == 0) {
+      F[rb] = (uint8_t)ftype;
+      sumA += (unsigned)ftype;
+      sumW += (unsigned long long)rb * (unsigned)ftype;
+    }
+    for (int cbase = 0; cbase < g.W; cbase += kChunkPx) {
+      const int c0 = cbase + lane * kLanePx;
+      uint32_t f[kLanePx];
+      const int n = residuals(g, r, c0, ftype, f);
+      for (int k = 0; k < 4 * n; k++) {
+        const unsigned v = (f[k >> 2] >> (8 * (k & 3))) & 255u;
+        const int64_t pos = rb + 1 + 4 * (int64_t)c0 + k;
+        F[pos] = (uint8_t)v;
+        sumA += v;
+        sumW += (unsigned long long)pos * v;
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     sumA += __shfl_xor_sync(0xffffffffu, sumA, o);
     sumW += __shfl_xor_sync(0xffffffffu, sumW, o);
   }
   if (lane == 0) {
-    atomicAdd(&s_adA, sumA);
-    atomicAdd(&s_adB, sumW);
+    atomicAdd(&s_a, sumA);
+    atomicAdd(&s_w, sumW);
   }
+  // zero the chunks' bucket tables (positions are stored + 1; 0 = empty)
+  uint4* tab = reinterpret_cast<uint4*>(base + b.lay.tab_off);
+  const int64_t nt = (int64_t)b.lay.nchunks * kBuckets;
+  for (int64_t i = threadIdx.x; i < nt; i += kPngThreads) tab[i] = make_uint4(0, 0, 0, 0);
+  for (int k = 0; k < 8; k++)
+    if (threadIdx.x == k) F[b.lay.nbytes + k] = 0;  // compare slack
   __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive scan of the row bits
-    uint64_t acc = 3;  // BFINAL + BTYPE
-    for (int r = 0; r < H; r++) {
-      const uint64_t b = s_rows[r];
-      s_rows[r] = acc;
-      acc += b;
+  if (threadIdx.x == 0) {
+    const unsigned long long N = (unsigned long long)b.lay.nbytes;
+    const uint32_t A = (uint32_t)((1 + s_a) % 65521ULL);
+    const uint32_t B = (uint32_t)((N + N * s_a - s_w) % 65521ULL);  // N + sum_i (N - i) d_i
+    *reinterpret_cast<uint32_t*>(base + b.lay.meta_off) = (B << 16) | A;
+  }
+}
+
+// ---- kernel 2: LZ77 parse, one warp per chunk ------------------------------
+__device__ __forceinline__ uint32_t hash3(const uint8_t* F, int64_t p) {
+  const uint32_t v = (uint32_t)F[p] | ((uint32_t)F[p + 1] << 8) | ((uint32_t)F[p + 2] << 16);
+  return (v * 2654435761u) >> (32 - 10);  // kBuckets = 2^10
+}
+
+// 4 bytes of F starting at byte x (little endian; F is 4-byte aligned and
+// padded, so the word after the last is readable)
+__device__ __forceinline__ uint32_t load4(const uint8_t* F, int64_t x) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(F) + (x >> 2);
+  return __funnelshift_r(__ldg(w), __ldg(w + 1), (unsigned)(x & 3) * 8);
+}
+
+// length of the common prefix of F[q..] and F[p..], capped at maxl
+__device__ __forceinline__ int match_len(const uint8_t* F, int64_t q, int64_t p, int maxl) {
+  int len = 0;
+  while (len < maxl) {
+    const uint32_t x = load4(F, q + len) ^ load4(F, p + len);
+    if (x) {
+      len += (__ffs(x) - 1) >> 3;
+      break;
     }
-    s_total = acc + 7;  // + end-of-block code (seven zero bits)
+    len += 4;
   }
-  __syncthreads();
-  const int64_t dbytes = (int64_t)((s_total + 7) / 8);
-  const int64_t zlen = 2 + dbytes + 4;
-  const int64_t file_len = kPrefix + zlen + 4 + 12;
-  if (file_len > cap) {  // cannot happen for cap = wg_png_capacity(W, H)
-    if (threadIdx.x == 0) lens[blockIdx.x] = -1;
+  return len < maxl ? len : maxl;
+}
+
+constexpr int kCands = kSlots + 6;
+
+// candidate k (0..kCands) for position p: the bucket's slots (as of the
+// current step), then the image-shaped distances 1, 4, row, 2 rows, row +- 4
+__device__ __forceinline__ int64_t candidate(const uint8_t* F, int64_t p, int k, int64_t S, const uint4* tab,
+                                             int64_t nbytes) {
+  if (k < kSlots) {
+    if (p + 2 >= nbytes) return -1;
+    const uint4 e = tab[hash3(F, p)];
+    const uint32_t v = k == 0 ? e.x : k == 1 ? e.y : k == 2 ? e.z : e.w;
+    return (int64_t)v - 1;
+  }
+  switch (k - kSlots) {
+    case 0: return p - 1;
+    case 1: return p - 4;
+    case 2: return p - S;
+    case 3: return p - 2 * S;
+    case 4: return p - S - 4;
+    default: return p - S + 4;
+  }
+}
+
+__device__ __forceinline__ bool valid_cand(int64_t q, int64_t p) { return q >= 0 && q < p && p - q <= kWindow; }
+
+// Greedy LZ77 over one chunk with a 32-position lookahead.  Phase 1: lane k
+// checks whether any candidate of position i + k shares its first 3 bytes;
+// the first such lane f ends the step (the lanes before it are literals),
+// so incompressible stretches advance 32 bytes per step.  Phase 2: lanes
+// 0..kCands-1 each extend one candidate of position i + f (4-byte
+// compares); the longest wins (ties: the earlier candidate).  Positions are
+// inserted after each step, one writer per bucket (deterministic).
+__global__ void __launch_bounds__(256) lz_kernel(Batch b, int64_t nwork) {
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wid >= nwork) return;
+  const int lane = threadIdx.x & 31;
+  const int img = (int)(wid / b.lay.nchunks), ch = (int)(wid % b.lay.nchunks);
+  uint8_t* base = b.scratch + (int64_t)img * b.lay.per_image;
+  const uint8_t* F = base + b.lay.f_off;
+  uint32_t* tok = reinterpret_cast<uint32_t*>(base + b.lay.tok_off);
+  uint4* tab = reinterpret_cast<uint4*>(base + b.lay.tab_off) + (int64_t)ch * kBuckets;
+  uint32_t* counts = reinterpret_cast<uint32_t*>(base + b.lay.meta_off + 8);
+  const int64_t S = 4 * (int64_t)b.W + 1;
+  const int64_t start = (int64_t)ch * b.lay.rows_per_chunk * S;
+  int64_t end = start + (int64_t)b.lay.rows_per_chunk * S;
+  if (end > b.lay.nbytes) end = b.lay.nbytes;
+  const int64_t nbytes = b.lay.nbytes;
+  int64_t ntok = 0;
+  uint32_t* out = tok + start;  // this chunk's tokens (at most one per byte)
+  int64_t i = start;
+  while (i < end) {
+    const int64_t p = i + lane;
+    bool quick = false;
+    if (p + 3 <= end) {
+      const uint32_t head = load4(F, p) & 0xFFFFFFu;
+      for (int k = 0; k < kCands && !quick; k++) {
+        const int64_t q = candidate(F, p, k, S, tab, nbytes);
+        quick = valid_cand(q, p) && (load4(F, q) & 0xFFFFFFu) == head;
+      }
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, quick);
+    const int nvalid = (int)min((int64_t)32, end - i);
+    const int f = hit ? __ffs(hit) - 1 : nvalid;  // literals before the first match
+    if (lane < f) out[ntok + lane] = F[p];
+    int64_t adv = f;
+    if (hit) {
+      const int64_t pf = i + f;
+      const int maxl = (int)(end - pf < 258 ? end - pf : 258);
+      int len = 0;
+      int64_t q = -1;
+      if (lane < kCands) {
+        q = candidate(F, pf, lane, S, tab, nbytes);
+        if (valid_cand(q, pf)) len = match_len(F, q, pf, maxl);
+      }
+      const unsigned key = ((unsigned)len << 8) | (unsigned)(31 - lane);
+      unsigned best = key;
+      for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      const int mlen = (int)(best >> 8);
+      const int64_t mq = __shfl_sync(0xffffffffu, q, 31 - (int)(best & 255u));
+      if (lane == 0) out[ntok + f] = ((uint32_t)mlen << 16) | (uint32_t)(pf - mq - 1);
+      ntok += f + 1;
+      adv += mlen;
+    } else {
+      ntok += f;
+    }
+    // insert the consumed positions (the first 32), newest per bucket wins
+    const int nins = adv < 32 ? (int)adv : 32;
+    const bool ins = lane < nins && p + 2 < nbytes;
+    const uint32_t h = ins ? hash3(F, p) : 0xFFFFFFFFu - lane;
+    const unsigned grp = __match_any_sync(0xffffffffu, h);
+    if (ins && (31 - __clz(grp)) == lane) {
+      const uint4 e = tab[h];
+      tab[h] = make_uint4((uint32_t)(p + 1), e.x, e.y, e.z);
+    }
+    __syncwarp();
+    i += adv;
+  }
+  if (lane == 0) counts[ch] = (uint32_t)ntok;
+}
+
+// ---- dynamic Huffman codes (RFC 1951 3.2.7), built by one thread ----------
+// Moffat-Katajainen in-place minimum-redundancy lengths: A[0..n) ascending
+// frequencies in, code lengths out.
+__device__ void min_redundancy(int* A, int n) {
+  if (n == 0) return;
+  if (n == 1) {
+    A[0] = 1;
     return;
   }
-  // zero the words the deflate bits go to, then the fixed prefix
+  A[0] += A[1];
+  int root = 0, leaf = 2, next;
+  for (next = 1; next < n - 1; next++) {
+    if (leaf >= n || A[root] < A[leaf]) {
+      A[next] = A[root];
+      A[root++] = next;
+    } else {
+      A[next] = A[leaf++];
+    }
+    if (leaf >= n || (root < next && A[root] < A[leaf])) {
+      A[next] += A[root];
+      A[root++] = next;
+    } else {
+      A[next] += A[leaf++];
+    }
+  }
+  A[n - 2] = 0;
+  for (next = n - 3; next >= 0; next--) A[next] = A[A[next]] + 1;
+  int avbl = 1, used = 0, dpth = 0;
+  root = n - 2;
+  next = n - 1;
+  while (avbl > 0) {
+    while (root >= 0 && A[root] == dpth) {
+      used++;
+      root--;
+    }
+    while (avbl > used) {
+      A[next--] = dpth;
+      avbl--;
+    }
+    avbl = 2 * used;
+    dpth++;
+    used = 0;
+  }
+}
+
+// Code lengths (<= limit) for freq[0..n); `complete`: the code must be
+// complete (lit/len, code-length code); otherwise a single used symbol gets
+// length 1 (the distance code's allowed incomplete case).  Scratch: sym, a
+// (n ints each).
+__device__ void build_lengths(const uint32_t* freq, int n, int limit, bool complete, uint8_t* len, int* sym, int* a) {
+  int m = 0;
+  for (int i = 0; i < n; i++) {
+    len[i] = 0;
+    if (freq[i]) sym[m++] = i;
+  }
+  if (m == 0) return;
+  if (m == 1) {
+    len[sym[0]] = 1;
+    if (complete) len[sym[0] == 0 ? 1 : 0] = 1;  // a dummy second code keeps it complete
+    return;
+  }
+  for (int i = 1; i < m; i++) {  // insertion sort by (freq, symbol) ascending
+    const int s = sym[i];
+    int j = i - 1;
+    while (j >= 0 && (freq[sym[j]] > freq[s] || (freq[sym[j]] == freq[s] && sym[j] > s))) {
+      sym[j + 1] = sym[j];
+      j--;
+    }
+    sym[j + 1] = s;
+  }
+  for (int i = 0; i < m; i++) a[i] = (int)freq[sym[i]];
+  min_redundancy(a, m);
+  int num[33] = {0};
+  for (int i = 0; i < m; i++) num[a[i] > 32 ? 32 : a[i]]++;
+  // enforce the limit (miniz's method on the per-length counts)
+  for (int i = limit + 1; i <= 32; i++) {
+    num[limit] += num[i];
+    num[i] = 0;
+  }
+  uint32_t total = 0;
+  for (int i = limit; i > 0; i--) total += (uint32_t)num[i] << (limit - i);
+  while (total != (1u << limit)) {
+    num[limit]--;
+    for (int i = limit - 1; i > 0; i--)
+      if (num[i]) {
+        num[i]--;
+        num[i + 1] += 2;
+        break;
+      }
+    total--;
+  }
+  // most frequent symbols get the shortest lengths
+  int j = m;
+  for (int l = 1; l <= limit; l++)
+    for (int c = num[l]; c > 0; c--) len[sym[--j]] = (uint8_t)l;
+}
+
+// canonical codes (RFC 1951 3.2.2), bit-reversed for LSB-first packing
+__device__ void canonical(const uint8_t* len, int n, uint16_t* code) {
+  int count[16] = {0};
+  for (int i = 0; i < n; i++) count[len[i]]++;
+  count[0] = 0;
+  int next[16];
+  int c = 0;
+  for (int bits = 1; bits < 16; bits++) {
+    c = (c + count[bits - 1]) << 1;
+    next[bits] = c;
+  }
+  for (int i = 0; i < n; i++)
+    if (len[i]) code[i] = (uint16_t)rev((uint32_t)next[len[i]]++, len[i]);
+}
+
+__device__ __forceinline__ unsigned len_sym(unsigned L, unsigned& extra, int& ebits) {
+  extra = 0;
+  ebits = 0;
+  if (L == 258) return 285;
+  if (L <= 10) return 254 + L;
+  const unsigned l = L - 3;
+  const int eb = 31 - __clz(l) - 2;
+  extra = l & ((1u << eb) - 1);
+  ebits = eb;
+  return 265 + (eb - 1) * 4 + ((l >> eb) - 4);
+}
+
+__device__ __forceinline__ unsigned dist_sym(unsigned d, unsigned& extra, int& ebits) {
+  extra = 0;
+  ebits = 0;
+  if (d <= 4) return d - 1;
+  const unsigned l = d - 1;
+  const int eb = 31 - __clz(l) - 1;
+  extra = l & ((1u << eb) - 1);
+  ebits = eb;
+  return 2 * (eb + 1) + ((l >> eb) & 1);
+}
+
+struct Codes {
+  uint16_t lit[286];
+  uint8_t litlen[286];
+  uint16_t dist[30];
+  uint8_t distlen[30];
+};
+
+__device__ __forceinline__ int dyn_bits(const Codes& c, uint32_t t) {
+  if (t < 256) return c.litlen[t];
+  unsigned e;
+  int eb, db;
+  const unsigned ls = len_sym(t >> 16, e, eb);
+  const unsigned ds = dist_sym((t & 0xFFFF) + 1, e, db);
+  return c.litlen[ls] + eb + c.distlen[ds] + db;
+}
+
+template <bool kWrite>
+__device__ __forceinline__ void dyn_put(Bits<kWrite>& o, const Codes& c, uint32_t t) {
+  if (t < 256) {
+    o.put(c.lit[t], c.litlen[t]);
+    return;
+  }
+  unsigned e;
+  int eb;
+  const unsigned ls = len_sym(t >> 16, e, eb);
+  o.put(c.lit[ls] | (e << c.litlen[ls]), c.litlen[ls] + eb);
+  const unsigned ds = dist_sym((t & 0xFFFF) + 1, e, eb);
+  o.put(c.dist[ds] | (e << c.distlen[ds]), c.distlen[ds] + eb);
+}
+
+__device__ const uint8_t kClOrder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+
+// The dynamic block: codes built once from the histograms (one thread),
+// then the header written or counted from the stored description.
+struct DynHeader {
+  Codes c;
+  uint8_t seq_sym[320], seq_ext[320];
+  int ns, hlit, hdist, hclen;
+  uint8_t cll[19];
+  uint16_t clc[19];
+};
+
+__device__ void dyn_build(DynHeader& h, const uint32_t* lf, const uint32_t* df, int* s1, int* s2) {
+  Codes& c = h.c;
+  build_lengths(lf, 286, 15, true, c.litlen, s1, s2);
+  build_lengths(df, 30, 15, false, c.distlen, s1, s2);
+  canonical(c.litlen, 286, c.lit);
+  canonical(c.distlen, 30, c.dist);
+  int hlit = 286;
+  while (hlit > 257 && c.litlen[hlit - 1] == 0) hlit--;
+  int hdist = 30;
+  while (hdist > 1 && c.distlen[hdist - 1] == 0) hdist--;
+  // run-length code the lengths (code-length alphabet 0..18)
+  uint8_t all[316];
+  for (int i = 0; i < hlit; i++) all[i] = c.litlen[i];
+  for (int i = 0; i < hdist; i++) all[hlit + i] = c.distlen[i];
+  const int n = hlit + hdist;
+  int ns = 0;
+  uint32_t clf[19] = {0};
+  for (int i = 0; i < n;) {
+    const uint8_t v = all[i];
+    int run = 1;
+    while (i + run < n && all[i + run] == v) run++;
+    int r = run;
+    if (v == 0) {
+      while (r >= 11) {
+        const int k = r < 138 ? r : 138;
+        h.seq_sym[ns] = 18, h.seq_ext[ns++] = (uint8_t)(k - 11), clf[18]++;
+        r -= k;
+      }
+      if (r >= 3) {
+        h.seq_sym[ns] = 17, h.seq_ext[ns++] = (uint8_t)(r - 3), clf[17]++;
+        r = 0;
+      }
+      for (; r > 0; r--) h.seq_sym[ns] = 0, h.seq_ext[ns++] = 0, clf[0]++;
+    } else {
+      h.seq_sym[ns] = v, h.seq_ext[ns++] = 0, clf[v]++;
+      r--;
+      while (r >= 3) {
+        const int k = r < 6 ? r : 6;
+        h.seq_sym[ns] = 16, h.seq_ext[ns++] = (uint8_t)(k - 3), clf[16]++;
+        r -= k;
+      }
+      for (; r > 0; r--) h.seq_sym[ns] = v, h.seq_ext[ns++] = 0, clf[v]++;
+    }
+    i += run;
+  }
+  build_lengths(clf, 19, 7, true, h.cll, s1, s2);
+  canonical(h.cll, 19, h.clc);
+  int hclen = 19;
+  while (hclen > 4 && h.cll[kClOrder[hclen - 1]] == 0) hclen--;
+  h.ns = ns;
+  h.hlit = hlit;
+  h.hdist = hdist;
+  h.hclen = hclen;
+}
+
+template <bool kWrite>
+__device__ uint64_t dyn_header(Bits<kWrite>& o, const DynHeader& h) {
+  const uint64_t p0 = o.pos;
+  o.put(0x5u, 3);  // BFINAL = 1, BTYPE = 10 (dynamic)
+  o.put((uint32_t)(h.hlit - 257), 5);
+  o.put((uint32_t)(h.hdist - 1), 5);
+  o.put((uint32_t)(h.hclen - 4), 4);
+  for (int i = 0; i < h.hclen; i++) o.put(h.cll[kClOrder[i]], 3);
+  for (int i = 0; i < h.ns; i++) {
+    const int sy = h.seq_sym[i];
+    o.put(h.clc[sy], h.cll[sy]);
+    if (sy == 16) o.put(h.seq_ext[i], 2);
+    if (sy == 17) o.put(h.seq_ext[i], 3);
+    if (sy == 18) o.put(h.seq_ext[i], 7);
+  }
+  return o.pos - p0;
+}
+
+// ---- kernel 3: codes, bits, zlib, checksums, chunks -----------------------
+__global__ void __launch_bounds__(kPngThreads) emit_kernel(Batch b) {
+  __shared__ uint32_t s_table[256];
+  __shared__ unsigned long long s_scan[kPngThreads];
+  __shared__ uint32_t s_lf[286], s_df[30];
+  __shared__ DynHeader s_dyn;
+  __shared__ int s_tmp1[288], s_tmp2[288];
+  __shared__ uint64_t s_hdr_bits;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* base = b.scratch + (int64_t)blockIdx.x * b.lay.per_image;
+  const uint32_t* tok = reinterpret_cast<const uint32_t*>(base + b.lay.tok_off);
+  const uint32_t* counts = reinterpret_cast<const uint32_t*>(base + b.lay.meta_off + 8);
+  uint8_t* img = b.out + (int64_t)blockIdx.x * b.cap;
+  const int64_t S = 4 * (int64_t)b.W + 1;
+  const int nch = b.lay.nchunks;
+  for (int i = threadIdx.x; i < 256; i += kPngThreads) s_table[i] = crc_table_entry((uint32_t)i);
+  for (int i = threadIdx.x; i < 286; i += kPngThreads) s_lf[i] = 0;
+  if (threadIdx.x < 30) s_df[threadIdx.x] = 0;
+  __syncthreads();
+  // histograms
+  for (int c = 0; c < nch; c++) {
+    const uint32_t* t = tok + (int64_t)c * b.lay.rows_per_chunk * S;
+    const int64_t n = counts[c];
+    for (int64_t k = threadIdx.x; k < n; k += kPngThreads) {
+      const uint32_t v = t[k];
+      if (v < 256) {
+        atomicAdd(&s_lf[v], 1u);
+      } else {
+        unsigned e;
+        int eb;
+        atomicAdd(&s_lf[len_sym(v >> 16, e, eb)], 1u);
+        atomicAdd(&s_df[dist_sym((v & 0xFFFF) + 1, e, eb)], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_lf[256] = 1;  // end of block
+    dyn_build(s_dyn, s_lf, s_df, s_tmp1, s_tmp2);
+    Bits<false> cnt{nullptr, 0};
+    s_hdr_bits = dyn_header(cnt, s_dyn);
+  }
+  __syncthreads();
+  const Codes& cd = s_dyn.c;
+  // pass 1: total bits
+  unsigned long long mine = 0;
+  for (int c = 0; c < nch; c++) {
+    const uint32_t* t = tok + (int64_t)c * b.lay.rows_per_chunk * S;
+    const int64_t n = counts[c];
+    for (int64_t k = threadIdx.x; k < n; k += kPngThreads) mine += (unsigned long long)dyn_bits(cd, t[k]);
+  }
+  s_scan[threadIdx.x] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int k = 0; k < kPngThreads; k++) tot += s_scan[k];
+    s_scan[0] = tot;
+  }
+  __syncthreads();
+  const uint64_t total_bits = s_hdr_bits + s_scan[0] + cd.litlen[256];
+  const int64_t dbytes = (int64_t)((total_bits + 7) / 8);
+  const int64_t zlen = 2 + dbytes + 4;
+  const int64_t file_len = kPrefix + zlen + 4 + 12;
+  __syncthreads();
+  if (file_len > b.cap) {  // dynamic codes lost to the worst-case bound: cannot happen in practice
+    if (threadIdx.x == 0) b.lens[blockIdx.x] = -1;
+    return;
+  }
   uint32_t* words = reinterpret_cast<uint32_t*>(img);
   const int64_t w_lo = (kPrefix + 2) / 4, w_hi = (kPrefix + 2 + dbytes + 3) / 4;
   for (int64_t w = w_lo + threadIdx.x; w < w_hi; w += kPngThreads) words[w] = 0u;
   __syncthreads();
+  const uint64_t bit_start = (uint64_t)(kPrefix + 2) * 8;
   if (threadIdx.x == 0) {
     const uint8_t sig[8] = {0x89, 'P', 'N', 'G', 0x0D, 0x0A, 0x1A, 0x0A};
     for (int i = 0; i < 8; i++) img[i] = sig[i];
     put_be32(img + 8, 13);
     img[12] = 'I', img[13] = 'H', img[14] = 'D', img[15] = 'R';
-    put_be32(img + 16, (uint32_t)W);
-    put_be32(img + 20, (uint32_t)H);
+    put_be32(img + 16, (uint32_t)b.W);
+    put_be32(img + 20, (uint32_t)b.H);
     img[24] = 8, img[25] = 6, img[26] = 0, img[27] = 0, img[28] = 0;  // 8-bit RGBA, deflate, adaptive, no interlace
     uint32_t c = 0xFFFFFFFFu;
     for (int i = 12; i < 29; i++) c = s_table[(c ^ img[i]) & 255u] ^ (c >> 8);
@@ -405,22 +862,39 @@ __global__ void __launch_bounds__(kPngThreads) png_kernel(const uint8_t* __restr
   }
   __threadfence();
   __syncthreads();
-  // ---- pass B: write the bits
-  const uint64_t bit0 = (uint64_t)(kPrefix + 2) * 8;
   if (threadIdx.x == 0) {
-    Bits<true> o{words, bit0};
-    o.put(0x3u, 3);  // BFINAL = 1, BTYPE = 01 (fixed Huffman)
+    Bits<true> o{words, bit_start};
+    dyn_header(o, s_dyn);
+    Bits<true> e{words, bit_start + total_bits - cd.litlen[256]};
+    e.put(cd.lit[256], cd.litlen[256]);  // end of block
   }
-  for (int r = warp; r < H; r += nw) visit_row<true>(g, r, words, bit0 + s_rows[r], sumA, sumW);
+  // pass 2: per chunk, block-scan the token bits and write them
+  uint64_t bit = bit_start + s_hdr_bits;
+  for (int c = 0; c < nch; c++) {
+    const uint32_t* t = tok + (int64_t)c * b.lay.rows_per_chunk * S;
+    const int64_t n = counts[c];
+    const int64_t per = (n + kPngThreads - 1) / kPngThreads;
+    const int64_t k0 = threadIdx.x * per < n ? threadIdx.x * per : n;
+    const int64_t k1 = k0 + per < n ? k0 + per : n;
+    unsigned long long m = 0;
+    for (int64_t k = k0; k < k1; k++) m += (unsigned long long)dyn_bits(cd, t[k]);
+    __syncthreads();
+    s_scan[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = 1; o < kPngThreads; o <<= 1) {
+      const unsigned long long y = threadIdx.x >= (unsigned)o ? s_scan[threadIdx.x - o] : 0;
+      __syncthreads();
+      s_scan[threadIdx.x] += y;
+      __syncthreads();
+    }
+    Bits<true> o{words, bit + s_scan[threadIdx.x] - m};
+    for (int64_t k = k0; k < k1; k++) dyn_put(o, cd, t[k]);
+    bit += s_scan[kPngThreads - 1];
+    __syncthreads();
+  }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {  // Adler-32 of the filtered data
-    const unsigned long long N = (unsigned long long)nbytes;
-    const uint32_t A = (uint32_t)((1 + s_adA) % 65521ULL);
-    // B = sum over k of (1 + bytes before k) = N + sum_i (N - i) d_i
-    const uint32_t B = (uint32_t)((N + N * s_adA - s_adB) % 65521ULL);
-    put_be32(img + kPrefix + 2 + dbytes, (B << 16) | A);
-  }
+  if (threadIdx.x == 0) put_be32(img + kPrefix + 2 + dbytes, *reinterpret_cast<const uint32_t*>(base + b.lay.meta_off));
   __threadfence();
   __syncthreads();
   if (warp == 0) {
@@ -431,21 +905,19 @@ __global__ void __launch_bounds__(kPngThreads) png_kernel(const uint8_t* __restr
       put_be32(e + 4, 0);
       e[8] = 'I', e[9] = 'E', e[10] = 'N', e[11] = 'D';
       put_be32(e + 12, 0xAE426082u);
-      lens[blockIdx.x] = file_len;
+      b.lens[blockIdx.x] = file_len;
     }
   }
 }
 
-int launch_png(const uint8_t* level, int64_t lw, int64_t lh, int64_t W, int64_t H, const int32_t* txy, int64_t n,
-               uint8_t* out, int64_t cap, int64_t* lens, cudaStream_t st) {
-  const size_t smem = (size_t)H * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
-    WG_CUDA_TRY(cudaFuncSetAttribute(png_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  png_kernel<<<(unsigned)n, kPngThreads, smem, st>>>(level, lw, lh, (int)W, (int)H, txy, out, cap, lens);
-  WG_LAUNCH_CHECK("png_kernel");
+int launch_png(Batch b, int64_t n, cudaStream_t st) {
+  filter_kernel<<<(unsigned)n, kPngThreads, 0, st>>>(b);
+  WG_LAUNCH_CHECK("filter_kernel");
+  const int64_t nwork = n * b.lay.nchunks;
+  lz_kernel<<<(unsigned)((nwork * 32 + 255) / 256), 256, 0, st>>>(b, nwork);
+  WG_LAUNCH_CHECK("lz_kernel");
+  emit_kernel<<<(unsigned)n, kPngThreads, 0, st>>>(b);
+  WG_LAUNCH_CHECK("emit_kernel");
   return WG_OK;
 }
 
@@ -454,32 +926,48 @@ int launch_png(const uint8_t* level, int64_t lw, int64_t lh, int64_t W, int64_t 
 extern "C" {
 
 int64_t wg_png_capacity(int64_t width, int64_t height) {
-  if (width < 1 || height < 1 || width > 0x7fffffff || height > 25000) return -1;
+  if (width < 1 || height < 1 || width > 0x7fffffff || height > 0x7fffffff) return -1;
   const int64_t raw = (4 * width + 1) * height;
-  const int64_t deflate = (raw * 9 + 3 + 7 + 7) / 8 + 8;  // <= 9 bits per byte
+  // fixed Huffman needs <= 9 bits per byte (a match never costs more than
+  // its literals); the dynamic code is optimal up to the length-limit
+  // adjustment, plus its header: a 1/64 + 4 KiB margin
+  const int64_t deflate = (raw * 9 + 3 + 7 + 7) / 8 + raw / 64 + 4096;
   return ((kPrefix + 2 + deflate + 4 + 4 + 12) + 255) / 256 * 256;
 }
 
+size_t wg_png_scratch_bytes(int64_t width, int64_t height, int64_t nimages) {
+  if (width < 1 || height < 1 || nimages < 0) return 0;
+  return (size_t)(layout_of(width, height).per_image * nimages);
+}
+
 int wg_png_tiles(const uint8_t* level, int64_t width, int64_t height, int64_t tile_px, const int32_t* txy,
-                 int64_t ntiles, uint8_t* out, int64_t cap, int64_t* lens, void* stream) {
+                 int64_t ntiles, uint8_t* out, int64_t cap, int64_t* lens, void* scratch, void* stream) {
   if (ntiles <= 0) return WG_OK;
   const int64_t need = wg_png_capacity(tile_px, tile_px);
-  if (need < 0) return wg::set_error(WG_EARG, "bad tile_px %lld", (long long)tile_px);
+  if (need < 0 || tile_px > 65535) return wg::set_error(WG_EARG, "bad tile_px %lld", (long long)tile_px);
   if (cap < need || cap % 4) return wg::set_error(WG_EARG, "per-tile capacity %lld < %lld", (long long)cap, (long long)need);
-  if (!level || !txy || !out || !lens || width < 1 || height < 1) return wg::set_error(WG_EARG, "bad arguments");
-  if ((((uintptr_t)level) & 3) || (((uintptr_t)out) & 3)) return wg::set_error(WG_EARG, "buffers must be 4-byte aligned");
+  if (!level || !txy || !out || !lens || !scratch || width < 1 || height < 1) return wg::set_error(WG_EARG, "bad arguments");
+  if ((((uintptr_t)level) & 3) || (((uintptr_t)out) & 3) || (((uintptr_t)scratch) & 255))
+    return wg::set_error(WG_EARG, "misaligned buffer");
   if (ntiles > 0x7fffffff) return wg::set_error(WG_ELIMIT, "too many tiles");
-  return launch_png(level, width, height, tile_px, tile_px, txy, ntiles, out, cap, lens, wg::as_stream(stream));
+  Batch b{level, width, height, (int)tile_px, (int)tile_px, txy, (uint8_t*)scratch, layout_of(tile_px, tile_px),
+          out, cap, lens};
+  if (b.lay.nchunks > 1024) return wg::set_error(WG_ELIMIT, "image too tall");
+  return launch_png(b, ntiles, wg::as_stream(stream));
 }
 
 int wg_png_encode(const uint8_t* pixels, int64_t width, int64_t height, uint8_t* out, int64_t cap, int64_t* len,
-                  void* stream) {
+                  void* scratch, void* stream) {
   const int64_t need = wg_png_capacity(width, height);
-  if (need < 0) return wg::set_error(WG_EARG, "bad image size %lldx%lld", (long long)width, (long long)height);
+  if (need < 0 || width > 65535 || height > 65535)
+    return wg::set_error(WG_EARG, "bad image size %lldx%lld", (long long)width, (long long)height);
   if (cap < need || cap % 4) return wg::set_error(WG_EARG, "capacity %lld < %lld", (long long)cap, (long long)need);
-  if (!pixels || !out || !len) return wg::set_error(WG_EARG, "null buffer");
-  if ((((uintptr_t)pixels) & 3) || (((uintptr_t)out) & 3)) return wg::set_error(WG_EARG, "buffers must be 4-byte aligned");
-  return launch_png(pixels, width, height, width, height, nullptr, 1, out, cap, len, wg::as_stream(stream));
+  if (!pixels || !out || !len || !scratch) return wg::set_error(WG_EARG, "null buffer");
+  if ((((uintptr_t)pixels) & 3) || (((uintptr_t)out) & 3) || (((uintptr_t)scratch) & 255))
+    return wg::set_error(WG_EARG, "misaligned buffer");
+  Batch b{pixels, width, height, (int)width, (int)height, nullptr, (uint8_t*)scratch, layout_of(width, height), out,
+          cap, len};
+  return launch_png(b, 1, wg::as_stream(stream));
 }
 
 }  // extern "C"

@@ -40,16 +40,17 @@ def gpu_encode(pyr, L, tile_px=256):
     bufs = {}
     for z, t in per_zoom.items():
         txy = torch.tensor([v for p in t for v in p], dtype=torch.int32, device="cuda")
-        bufs[z] = (txy, _device.empty((cap * len(t),), torch.uint8), _device.empty((len(t),), torch.int64))
+        bufs[z] = (txy, _device.empty((cap * len(t),), torch.uint8), _device.empty((len(t),), torch.int64),
+                   _device.empty((int(L.wg_png_scratch_bytes(tile_px, tile_px, len(t))),), torch.uint8))
     best = 1e30
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for z, t in per_zoom.items():
             level = pyr.levels[zmax - z].dev("pixels")
-            txy, out, lens = bufs[z]
+            txy, out, lens, sc = bufs[z]
             L.wg_png_tiles(_lib.ptr(level), int(level.shape[1]), int(level.shape[0]), tile_px, _lib.ptr(txy), len(t),
-                           _lib.ptr(out), cap, _lib.ptr(lens), _lib.stream_ptr())
+                           _lib.ptr(out), cap, _lib.ptr(lens), _lib.ptr(sc), _lib.stream_ptr())
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
