@@ -88,19 +88,26 @@ def run_avalanche(elev, ox, oy, cs, mask, *, persistence=0.9, randomness=0.16, r
 
 
 def run_range(elev, ox, oy, cs, cells, lo, hi, hits, zmax, *, persistence=0.9, randomness=0.16,
-              runout_angle_deg=25.0, particles_per_release_cell=2048, seed=0, max_steps=None, threads=None) -> int:
+              runout_angle_deg=25.0, particles_per_release_cell=2048, seed=0, max_steps=None, threads=None,
+              records=False):
     """Particles [lo, hi) accumulated into caller-owned rasters (one shared
     pair across calls, unlike the reference's per-chunk partials); returns
-    the particle steps taken."""
+    the particle steps taken, and with records=True also the per-particle
+    (reason, steps, end) arrays."""
     n = hi - lo
     if n <= 0:
-        return 0
+        return (0, None) if records else 0
     steps = np.zeros(n, dtype=np.int64)
+    reasons = np.zeros(n, dtype=np.int8) if records else None
+    ends = np.zeros((n, 2), dtype=np.float64) if records else None
     lib().orc_run_particles(
         *world_args(elev, ox, oy, cs, persistence, randomness, runout_angle_deg, max_steps),
         cells.ctypes.data, particles_per_release_cell, seed & MASK64, lo, hi, hits.ctypes.data, zmax.ctypes.data,
-        None, steps.ctypes.data, None, int(threads or os.cpu_count() or 1),
+        reasons.ctypes.data if records else None, steps.ctypes.data, ends.ctypes.data if records else None,
+        int(threads or os.cpu_count() or 1),
     )
+    if records:
+        return int(steps.sum()), (reasons, steps, ends)
     return int(steps.sum())
 
 
