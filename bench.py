@@ -375,8 +375,10 @@ def main() -> None:
     # overlay latency: full avalanche workflow through the Executor at the
     # largest size the reference's texture cap allows (configs[3]-like)
     overlay = None
+    snow = None
     if not a.no_overlay and rank == 0 and world == 1:
         overlay = overlay_latency(wf, a)
+        snow = snow_latency(wf)
 
     if rank == 0:
         pk = peaks()
@@ -415,6 +417,8 @@ def main() -> None:
         }
         if overlay is not None:
             line["overlay_latency_ms"] = overlay
+        if snow is not None:
+            line["snow_latency_ms"] = snow
         if not a.no_cpu:
             e, m = host_inputs(a)
             line["cpu_baseline"] = cpu_sample(e, m, a, a.cpu_chunks)
@@ -460,6 +464,37 @@ def overlay_latency(wf, a) -> dict:
                       "256 particles/cell, colorize + full mip",
             "cold": min(cold), "warm_steering": min(warm), "warm_cache_hits": rep.cache_hits,
             "stats": res.value("avalanche_overlay", "stats"), "node_ms_cold": nodes}
+
+
+def snow_latency(wf) -> dict:
+    """Cold latency of the stock snow graph at SURVEY §8d C2: synth_dem(4096, 0),
+    snow line at the median height, zoom 1 (4 tiles), full 13-level mip."""
+    import torch
+
+    from paper_2506_23364_b200.synth import synth_dem_device
+
+    n = 4096
+    z = synth_dem_device(n, 0)
+    world = wf.DemGrid(n, n, 0.0, 0.0, 10.0, -9999.0, z)
+    line = float(torch.median(z.view(-1)).item())
+    params = wf.SnowParams(snow_line_m=line, altitude_blend_m=200.0, max_steepness_deg=50.0, steepness_blend_deg=10.0)
+
+    def graph():
+        g = wf.build_snow_graph(world.extent, params, zoom=1)
+        g.bind("world", world)
+        return g
+
+    wf.Executor().execute(graph())  # warm
+    torch.cuda.synchronize()
+    cold = []
+    for _ in range(3):
+        ex = wf.Executor()
+        t0 = time.perf_counter()
+        res = ex.execute(graph())
+        cold.append((time.perf_counter() - t0) * 1e3)
+    nodes = {r.node_id: round(r.elapsed_ms, 3) for r in res.report.records}
+    return {"config": "stock snow graph (6 nodes), synth_dem(4096, 0), snow line = median height, zoom 1, 13-level mip",
+            "cold": min(cold), "node_ms_cold": nodes}
 
 
 if __name__ == "__main__":
