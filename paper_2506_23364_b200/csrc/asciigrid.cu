@@ -29,27 +29,52 @@ constexpr int kFmtMax = 25;  // longest format_number output (24) + separator
 
 __device__ __forceinline__ bool is_ws(unsigned c) { return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f); }
 
-// token-start bits of this thread's 16 bytes [p0, p0 + 16) within [lo, n)
+// whitespace bytes of a 32-bit word as 0xFF bytes (SWAR): space, \t..\r,
+// \x1c..\x1f
+__device__ __forceinline__ unsigned ws_bytes(unsigned w) {
+  return __vcmpeq4(w, 0x20202020u) | __vcmpltu4(__vsub4(w, 0x09090909u), 0x05050505u) |
+         __vcmpltu4(__vsub4(w, 0x1c1c1c1cu), 0x04040404u);
+}
+
+// one bit per byte (byte k -> bit k) of a 0x00/0xFF byte mask
+__device__ __forceinline__ unsigned byte_bits(unsigned m) { return ((m & 0x01010101u) * 0x01020408u) >> 24; }
+
+// token-start bits of this thread's 16 bytes [p0, p0 + 16) within [lo, n):
+// SWAR classification of four words; bytes outside [lo, n) count as
+// whitespace; the byte before p0 comes from the previous lane (lane 0 loads it)
 __device__ __forceinline__ unsigned start_bits(const unsigned char* __restrict__ t, int64_t p0, int64_t lo, int64_t n,
                                                unsigned& nonascii) {
-  unsigned char b[kTokBytes];
-  if (p0 + kTokBytes <= n && ((reinterpret_cast<uintptr_t>(t + p0) & 15) == 0)) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(t + p0));
-    *reinterpret_cast<uint4*>(b) = v;
+  uint4 v;
+  if (p0 + kTokBytes <= n) {
+    v = __ldg(reinterpret_cast<const uint4*>(t + p0));
   } else {
+    unsigned char b[kTokBytes];
     for (int k = 0; k < kTokBytes; k++) b[k] = (p0 + k < n) ? __ldg(t + p0 + k) : ' ';
+    v = *reinterpret_cast<const uint4*>(b);
   }
-  unsigned prev_ws = (p0 <= lo) ? 1u : (is_ws(__ldg(t + p0 - 1)) ? 1u : 0u);
-  unsigned bits = 0;
-  for (int k = 0; k < kTokBytes; k++) {
-    const unsigned c = b[k];
-    const bool in = p0 + k >= lo && p0 + k < n;
-    const bool ws = is_ws(c);
-    if (in && !ws && prev_ws) bits |= 1u << k;
-    if (in) nonascii |= c >> 7;
-    prev_ws = ws ? 1u : 0u;
+  unsigned ws = byte_bits(ws_bytes(v.x)) | (byte_bits(ws_bytes(v.y)) << 4) | (byte_bits(ws_bytes(v.z)) << 8) |
+                (byte_bits(ws_bytes(v.w)) << 12);
+  unsigned hi = (v.x | v.y | v.z | v.w) & 0x80808080u;
+  if (p0 < lo) {  // header bytes: neither tokens nor body
+    const int64_t k = lo - p0;
+    const unsigned out = k >= kTokBytes ? 0xFFFFu : ((1u << k) - 1u);
+    ws |= out;
+    if (k >= kTokBytes) hi = 0;
+    else {
+      const unsigned char* pb = reinterpret_cast<const unsigned char*>(&v);
+      hi = 0;
+      for (int q = (int)k; q < kTokBytes; q++) hi |= pb[q] & 0x80u;
+    }
   }
-  return bits;
+  if (p0 + kTokBytes > n) {
+    const int64_t k = n - p0;  // in-range bytes (< 16)
+    ws |= k <= 0 ? 0xFFFFu : (0xFFFFu << k) & 0xFFFFu;
+  }
+  nonascii |= hi ? 1u : 0u;
+  const int lane = threadIdx.x & 31;
+  unsigned prev = __shfl_up_sync(0xffffffffu, ws >> 15, 1);
+  if (lane == 0) prev = (p0 <= lo) ? 1u : (is_ws(__ldg(t + p0 - 1)) ? 1u : 0u);
+  return ~ws & ((ws << 1) | prev) & 0xFFFFu;
 }
 
 __global__ void tok_count_kernel(const unsigned char* __restrict__ t, int64_t lo, int64_t n,
@@ -123,16 +148,70 @@ __global__ void tok_scatter_kernel(const unsigned char* __restrict__ t, int64_t 
   }
 }
 
+// Fast path for the common numeral shape [+-]digits[.digits] (no exponent,
+// no underscore, <= 19 significant digits): the token's bytes come from six
+// word loads held in registers, the token end from a SWAR whitespace scan,
+// and the value from the same Eisel-Lemire conversion nc_parse uses.  Any
+// other shape (or a token near the end of the text) returns false and the
+// caller runs the general nc_parse.
+__device__ __forceinline__ bool parse_fast(const unsigned char* __restrict__ t, int64_t s, int64_t n, double* v,
+                                           int64_t* len_out) {
+  if (s + 28 > n) return false;
+  uint32_t w[6];
+  const uint32_t* base = reinterpret_cast<const uint32_t*>(t) + (s >> 2);
+  const unsigned sh = (unsigned)(s & 3) * 8;
+#pragma unroll
+  for (int k = 0; k < 6; k++) w[k] = __funnelshift_r(__ldg(base + k), __ldg(base + k + 1), sh);
+  unsigned wsm = 0;
+#pragma unroll
+  for (int k = 0; k < 6; k++) wsm |= byte_bits(ws_bytes(w[k])) << (4 * k);
+  if (wsm == 0) return false;  // token of 24+ bytes
+  const int len = __ffs(wsm) - 1;
+  *len_out = len;
+  const unsigned c0 = w[0] & 255u;
+  const bool neg = c0 == '-';
+  const int k0 = (c0 == '-' || c0 == '+') ? 1 : 0;
+  uint64_t m = 0;
+  int kept = 0, frac = 0;
+  bool dot = false, any = false, bad = false;
+#pragma unroll
+  for (int k = 0; k < 24; k++) {  // fully unrolled: the bytes stay in registers
+    if (k >= k0 && k < len) {
+      const unsigned c = (w[k >> 2] >> (8 * (k & 3))) & 255u;
+      const unsigned d = c - '0';
+      if (d <= 9) {
+        any = true;
+        if (m != 0 || d != 0) {
+          bad |= kept == 19;
+          m = m * 10 + d;
+          kept++;
+        }
+        frac += dot ? 1 : 0;
+      } else {
+        bad |= !(c == '.' && !dot);
+        dot = true;
+      }
+    }
+  }
+  if (bad || !any) return false;
+  const uint64_t bits = m == 0 ? 0 : nc::el_convert(-(int64_t)frac, m, (const uint64_t(*)[2])kEL);
+  *v = nc::bits_to_double(bits | (neg ? 0x8000000000000000ULL : 0));
+  return true;
+}
+
 __global__ void parse_kernel(const unsigned char* __restrict__ t, int64_t n, const int64_t* __restrict__ starts,
                              int64_t count, double* __restrict__ out, unsigned long long* __restrict__ first_bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = starts[i];
-    int64_t e = s;
-    while (e < n && !is_ws(__ldg(t + e))) e++;
-    const int64_t len = e - s;
     double v = 0.0;
-    const int rc = len > 0x7fffffff ? -1 : nc::nc_parse(t + s, (int)len, &v, (const uint64_t(*)[2])kEL);
-    if (rc != 0) atomicMin(first_bad, (unsigned long long)i);
+    int64_t len;
+    if (!parse_fast(t, s, n, &v, &len)) {
+      int64_t e = s;
+      while (e < n && !is_ws(__ldg(t + e))) e++;
+      len = e - s;
+      const int rc = len > 0x7fffffff ? -1 : nc::nc_parse(t + s, (int)len, &v, (const uint64_t(*)[2])kEL);
+      if (rc != 0) atomicMin(first_bad, (unsigned long long)i);
+    }
     out[i] = v;
   }
 }
