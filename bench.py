@@ -44,7 +44,7 @@ BYTES_PER_STEP = 64  # 32 B DEM patch + 16 B hit RMW + 16 B drop
 FP64_OPS_PER_STEP = 180  # 154 DFMA+DMUL+DADD + 26 DSETP (ncu source page, r01 final build)
 FP64_PEAK_OPS = 1.853e13
 # DRAM bytes per traj_kernel launch from ncu --set full (dram__bytes_read+write, r01)
-TRAJ_DRAM_BYTES = 6.36e9
+TRAJ_DRAM_BYTES = 6.65e9
 
 
 def parse():
