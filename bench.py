@@ -262,7 +262,7 @@ def main() -> None:
         run_avalanche_device(g, cells, params, rank=rank, nranks=world, hits=hits, zmax=zmax)
         e1.record(stream)
         if world > 1:
-            merge_runout(hits, zmax)
+            merge_runout(hits, zmax, dst=0)  # rank 0 holds the overlay (stats below are rank 0's)
         run = wf.RunoutRaster(zmax, hits)  # invariants + stats pass
         return run, mask, (e0, e1)
 

@@ -6,8 +6,8 @@ any partition of the particle index space yields the bitwise-identical
 raster.  Each rank runs the trajectory kernel on its blocked-cyclic share of
 release-point blocks (csrc/traj.cu, ``rank``/``nranks``/``shard_block``)
 into a private int64 hit raster and float64 drop raster; this module merges
-them with one NCCL all-reduce each (SUM for hits, MAX for drops) over
-NVLink/NVSwitch.  Under the gloo backend (CPU tests) the same calls run on
+them with one NCCL all-reduce (or reduce to one rank) each (SUM for hits,
+MAX for drops) over NVLink/NVSwitch.  Under the gloo backend (CPU tests) the same calls run on
 host tensors.
 """
 
@@ -42,7 +42,14 @@ def local_indices(total: int, block: int, rank: int, nranks: int) -> list[range]
     return out
 
 
-def merge_runout(hits: torch.Tensor, zmax: torch.Tensor, group=None) -> None:
-    """In-place all-reduce of one rank's private rasters: hits SUM, drops MAX."""
-    dist.all_reduce(hits, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(zmax, op=dist.ReduceOp.MAX, group=group)
+def merge_runout(hits: torch.Tensor, zmax: torch.Tensor, group=None, dst: int | None = None) -> None:
+    """In-place merge of one rank's private rasters: hits SUM, drops MAX.
+    All ranks receive the result (all-reduce), or only rank `dst` (reduce:
+    half the NVLink traffic when one rank colorizes the overlay, as the
+    reference's single process does)."""
+    if dst is None:
+        dist.all_reduce(hits, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(zmax, op=dist.ReduceOp.MAX, group=group)
+    else:
+        dist.reduce(hits, dst, op=dist.ReduceOp.SUM, group=group)
+        dist.reduce(zmax, dst, op=dist.ReduceOp.MAX, group=group)

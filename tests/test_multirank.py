@@ -36,9 +36,13 @@ def _worker(rank, world, port, elev, mask, out):
             traj.run_range(elev, 0.0, 0.0, 10.0, cells, rg.start, rg.stop, hits, zmax, particles_per_release_cell=ppc,
                            seed=4, threads=2)
         h, z = torch.from_numpy(hits), torch.from_numpy(zmax)
-        merge_runout(h, z)
+        h2, z2 = h.clone(), z.clone()
+        merge_runout(h, z)  # all-reduce: every rank holds the merged raster
+        merge_runout(h2, z2, dst=0)  # reduce: rank 0 only (the bench's N>1 path)
         if rank == 0:
-            out.put((h.numpy().copy(), z.numpy().copy()))
+            out.put((h.numpy().copy(), z.numpy().copy(), h2.numpy().copy(), z2.numpy().copy()))
+        else:
+            out.put((h.numpy().copy(), z.numpy().copy(), None, None))
     finally:
         dist.destroy_process_group()
 
@@ -56,10 +60,15 @@ def test_two_rank_merge_equals_single_run():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, elev, mask, q)) for r in range(2)]
     for p in procs:
         p.start()
-    h, z = q.get(timeout=300)
+    got = [q.get(timeout=300) for _ in range(2)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     z1, h1 = traj.run_avalanche(elev, 0.0, 0.0, 10.0, mask, particles_per_release_cell=96, seed=4)
-    assert np.array_equal(h, h1)
-    assert np.array_equal(z.view(np.int64), z1.view(np.int64))
+    for h, z, h2, z2 in got:  # all-reduce: both ranks
+        assert np.array_equal(h, h1)
+        assert np.array_equal(z.view(np.int64), z1.view(np.int64))
+    roots = [(h2, z2) for _, _, h2, z2 in got if h2 is not None]
+    assert len(roots) == 1  # reduce: the root's rasters
+    assert np.array_equal(roots[0][0], h1)
+    assert np.array_equal(roots[0][1].view(np.int64), z1.view(np.int64))
