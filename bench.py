@@ -233,10 +233,16 @@ def main() -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # WG_BENCH_BACKEND=gloo: code-path check of the N>1 bench with every rank
+    # on one GPU (NCCL refuses two ranks per device); never a measurement
+    backend = os.environ.get("WG_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     _lib.build()
     L = _lib.lib()
     dev = torch.device("cuda", local)
@@ -246,6 +252,10 @@ def main() -> None:
     grid = wf.DemGrid(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, elev_dev)
     params = wf.AvalancheParams(particles_per_release_cell=a.ppc, seed=a.seed)
     traj_ms: list[float] = []
+    # N > 1: step i's overlay merge (NCCL reduce to rank 0 + stats) runs on its
+    # own stream, overlapping step i+1's upstream nodes and trajectories
+    # (two raster generations in HBM; not at C5, where one is 64 GiB)
+    merge_stream = torch.cuda.Stream() if world > 1 and a.config != "c5" else None
 
     def hot_path(g):
         if a.slope_only:
@@ -261,8 +271,16 @@ def main() -> None:
         e0.record(stream)
         run_avalanche_device(g, cells, params, rank=rank, nranks=world, hits=hits, zmax=zmax)
         e1.record(stream)
+        if merge_stream is not None:
+            merge_stream.wait_stream(stream)
+            with torch.cuda.stream(merge_stream):
+                merge_runout(hits, zmax, dst=0)  # rank 0 holds the overlay
+                run = wf.RunoutRaster(zmax, hits, _deferred=True)  # invariants + stats pass, read lazily
+            hits.record_stream(merge_stream)
+            zmax.record_stream(merge_stream)
+            return run, mask, (e0, e1)
         if world > 1:
-            merge_runout(hits, zmax, dst=0)  # rank 0 holds the overlay (stats below are rank 0's)
+            merge_runout(hits, zmax, dst=0)
         run = wf.RunoutRaster(zmax, hits)  # invariants + stats pass
         return run, mask, (e0, e1)
 
@@ -280,6 +298,10 @@ def main() -> None:
         run, mask, ev = hot_path(grid)
     released = wf.simulate.released_particles(mask, params)
     total_steps = run.total_hits - released
+    if world > 1:  # only rank 0 holds the merged overlay (reduce)
+        tt = torch.tensor([total_steps], dtype=torch.int64, device=dev)
+        dist.broadcast(tt, 0)
+        total_steps = int(tt.item())
 
     # timed: device-resident
     barrier()
@@ -293,6 +315,8 @@ def main() -> None:
             run = mask = None
             run, mask, ev = hot_path(grid)
             evs.append(ev)
+        if merge_stream is not None:
+            stream.wait_stream(merge_stream)  # the last merge is inside the timed region
         t1.record(stream)
         barrier()
     launches = _lib.launch_count() - launches0
@@ -388,8 +412,10 @@ def main() -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "backend": backend if world > 1 else None,
             "config": {**workload(a), "parallelism": f"particles sharded by release-point blocks over {world} GPU(s), "
-                                                      "NCCL all-reduce of the overlay"},
+                                                      "NCCL reduce of the overlay to rank 0 overlapped with the "
+                                                      "next step"},
             "particle_steps_per_step": total_steps,
             "released_particles": released,
             "traj_kernel_ms": traj_avg,
