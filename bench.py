@@ -226,7 +226,7 @@ def main() -> None:
 
     import paper_2506_23364_b200 as wf
     from paper_2506_23364_b200 import _lib
-    from paper_2506_23364_b200.shard import merge_runout
+    from paper_2506_23364_b200.shard import merge_runout, release_cells_banded
     from paper_2506_23364_b200.simulate import release_cells, run_avalanche_device
     from paper_2506_23364_b200.synth import synth_dem_device
     from paper_2506_23364_b200.terrain import compute_normals_and_slope, compute_slope
@@ -256,14 +256,20 @@ def main() -> None:
     # own stream, overlapping step i+1's upstream nodes and trajectories
     # (two raster generations in HBM; not at C5, where one is 64 GiB)
     merge_stream = torch.cuda.Stream() if world > 1 and a.config != "c5" else None
+    merge_ev: list = []
 
     def hot_path(g):
-        if a.slope_only:
-            slope = compute_slope(g)
+        if world > 1:
+            # upstream nodes sharded by row band, cell lists all-gathered
+            cells = release_cells_banded(g, 30.0, 45.0, a.stride, rank, world, with_normals=not a.slope_only)
         else:
-            _, slope = compute_normals_and_slope(g)
-        mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
-        cells = release_cells(mask)
+            if a.slope_only:
+                slope = compute_slope(g)
+            else:
+                _, slope = compute_normals_and_slope(g)
+            mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
+            del slope
+            cells = release_cells(mask)
         hits = torch.zeros((g.nrows, g.ncols), dtype=torch.int64, device=dev)
         zmax = torch.zeros((g.nrows, g.ncols), dtype=torch.float64, device=dev)
         e0 = torch.cuda.Event(enable_timing=True)
@@ -273,16 +279,21 @@ def main() -> None:
         e1.record(stream)
         if merge_stream is not None:
             merge_stream.wait_stream(stream)
+            m0 = torch.cuda.Event(enable_timing=True)
+            m1 = torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(merge_stream):
+                m0.record(merge_stream)
                 merge_runout(hits, zmax, dst=0)  # rank 0 holds the overlay
+                m1.record(merge_stream)
+                merge_ev.append((m0, m1))
                 run = wf.RunoutRaster(zmax, hits, _deferred=True)  # invariants + stats pass, read lazily
             hits.record_stream(merge_stream)
             zmax.record_stream(merge_stream)
-            return run, mask, (e0, e1)
+            return run, cells, (e0, e1)
         if world > 1:
             merge_runout(hits, zmax, dst=0)
         run = wf.RunoutRaster(zmax, hits)  # invariants + stats pass
-        return run, mask, (e0, e1)
+        return run, cells, (e0, e1)
 
     def barrier():
         torch.cuda.synchronize()
@@ -292,11 +303,11 @@ def main() -> None:
 
     # warm-up (drop the previous pass's rasters before the next allocates:
     # at 65536^2 two generations do not fit in HBM)
-    run = mask = None
+    run = cells = None
     for _ in range(a.warmup):
-        run = mask = None
-        run, mask, ev = hot_path(grid)
-    released = wf.simulate.released_particles(mask, params)
+        run = cells = None
+        run, cells, ev = hot_path(grid)
+    released = int(cells.numel()) * params.particles_per_release_cell
     total_steps = run.total_hits - released
     if world > 1:  # only rank 0 holds the merged overlay (reduce)
         tt = torch.tensor([total_steps], dtype=torch.int64, device=dev)
@@ -312,8 +323,8 @@ def main() -> None:
         t0.record(stream)
         evs = []
         for _ in range(a.steps):
-            run = mask = None
-            run, mask, ev = hot_path(grid)
+            run = cells = None
+            run, cells, ev = hot_path(grid)
             evs.append(ev)
         if merge_stream is not None:
             stream.wait_stream(merge_stream)  # the last merge is inside the timed region
@@ -326,7 +337,6 @@ def main() -> None:
     if world > 1:
         # this rank's share of the particle steps (for its own kernel roofline):
         # one untimed private-raster pass, read before any merge
-        cells = release_cells(mask)
         del run  # free the merged rasters first (64 GiB at 65536^2)
         torch.cuda.empty_cache()
         h = torch.zeros((a.size, a.size), dtype=torch.int64, device=dev)
@@ -338,9 +348,11 @@ def main() -> None:
             int(cells.numel()) * a.ppc, 2048, rank, world)
         del h, z
         # each rank's average launch, max over ranks
-        tt = torch.tensor([ms, sum(traj_ms) / len(traj_ms)], dtype=torch.float64, device=dev)
+        timed = merge_ev[-a.steps:]
+        merge_avg = sum(m0.elapsed_time(m1) for m0, m1 in timed) / len(timed) if timed else 0.0
+        tt = torch.tensor([ms, sum(traj_ms) / len(traj_ms), merge_avg], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, traj_avg = tt.tolist()
+        ms, traj_avg, merge_avg = tt.tolist()
     else:
         traj_avg = sum(traj_ms) / len(traj_ms)  # average launch duration (roofline contract)
     ms_per_step = ms / a.steps
@@ -419,6 +431,7 @@ def main() -> None:
             "particle_steps_per_step": total_steps,
             "released_particles": released,
             "traj_kernel_ms": traj_avg,
+            "merge_ms": merge_avg if world > 1 else None,
             "traj_kernel_ms_per_launch": [round(t, 3) for t in traj_ms],
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": cell_bytes, "d2h_bytes_per_step": 2 * cell_bytes,
