@@ -84,8 +84,8 @@ SIGNATURES: dict[str, tuple] = {
     "wg_ascii_tokenize": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_ascii_parse": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_ascii_format_scratch_bytes": (c_size, [c_i64]),
-    "wg_ascii_format_size": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
-    "wg_ascii_format_write": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
+    "wg_ascii_format_capacity": (c_i64, [c_i64]),
+    "wg_ascii_format": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
 }
 
 WG_OK, WG_ECUDA, WG_EARG, WG_ELIMIT = 0, 1, 2, 3

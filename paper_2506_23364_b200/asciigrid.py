@@ -209,12 +209,13 @@ def write_ascii_grid_bytes(grid: DemGrid) -> memoryview:
     count = v.numel()
     scratch = _device.empty((int(L.wg_ascii_format_scratch_bytes(count)),), torch.uint8)
     nb = _device.empty((1,), torch.int64)
-    _lib.check(L.wg_ascii_format_size(_lib.ptr(v), count, _lib.ptr(nb), _lib.ptr(scratch), _lib.stream_ptr()))
+    cap = int(L.wg_ascii_format_capacity(count))
+    full = _device.empty((len(head) + cap,), torch.uint8)  # upper bound; the used prefix is downloaded
+    full[: len(head)].copy_(torch.tensor(list(head), dtype=torch.uint8))
+    _lib.check(L.wg_ascii_format(_lib.ptr(v), count, grid.ncols, _lib.ptr(full[len(head):]), cap, _lib.ptr(nb),
+                                 _lib.ptr(scratch), _lib.stream_ptr()))
     nbytes = int(_device.read_small(nb)[0])
-    out = _device.empty((len(head) + nbytes,), torch.uint8)
-    out[: len(head)].copy_(torch.tensor(list(head), dtype=torch.uint8))
-    _lib.check(L.wg_ascii_format_write(_lib.ptr(v), count, grid.ncols, _lib.ptr(out[len(head):]), _lib.ptr(scratch),
-                                       _lib.stream_ptr()))
+    out = full[: len(head) + nbytes]
     # one pageable D2H straight into uninitialised host memory: at multi-GB
     # sizes first-touch page zeroing (~5 GB/s) bounds any strategy, and
     # bytearray's zero-fill or pinned staging only add to it

@@ -26,6 +26,7 @@ constexpr int kTokBytes = 16;  // per thread
 constexpr int64_t kTokTile = (int64_t)kTokThreads * kTokBytes;
 constexpr int kFmtThreads = 256;
 constexpr int kFmtMax = 25;  // longest format_number output (24) + separator
+constexpr int kFmtPer = 4;   // values per thread in the one-pass writer
 
 __device__ __forceinline__ bool is_ws(unsigned c) { return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f); }
 
@@ -95,29 +96,42 @@ __global__ void tok_count_kernel(const unsigned char* __restrict__ t, int64_t lo
   }
 }
 
-// exclusive scan of n counts in place (one block); total to *total
+// exclusive scan of n counts in place (one block of 1024); total to *total.
+// Per 1024-element chunk: warp shuffles, one shared pass over the 32 warp
+// sums, a running carry.
 __global__ void scan_kernel(unsigned long long* __restrict__ v, int64_t n, unsigned long long* __restrict__ total) {
-  __shared__ unsigned long long s[1024];
-  __shared__ unsigned long long carry;
-  if (threadIdx.x == 0) carry = 0;
+  __shared__ unsigned long long s_warp[32];
+  __shared__ unsigned long long s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
   __syncthreads();
   for (int64_t base = 0; base < n; base += 1024) {
     const int64_t i = base + threadIdx.x;
     const unsigned long long x = i < n ? v[i] : 0;
-    s[threadIdx.x] = x;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const unsigned long long y = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
-      __syncthreads();
-      s[threadIdx.x] += y;
-      __syncthreads();
+    unsigned long long y = x;  // inclusive warp scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
     }
-    if (i < n) v[i] = carry + s[threadIdx.x] - x;
+    if (lane == 31) s_warp[warp] = y;
     __syncthreads();
-    if (threadIdx.x == 1023) carry += s[1023];
+    if (warp == 0) {
+      const unsigned long long w = s_warp[lane];
+      unsigned long long z = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += t;
+      }
+      s_warp[lane] = z - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    const unsigned long long carry = s_carry;
+    if (i < n) v[i] = carry + s_warp[warp] + y - x;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = carry + s_warp[31] + y;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total = carry;
+  if (threadIdx.x == 0) *total = s_carry;
 }
 
 __global__ void tok_scatter_kernel(const unsigned char* __restrict__ t, int64_t lo, int64_t n,
@@ -220,36 +234,47 @@ __device__ __forceinline__ int format_value(double v, char* buf) {
   return nc::nc_format(v, buf, (const uint64_t(*)[2])kPow5Inv, (const uint64_t(*)[2])kPow5);
 }
 
-// pass 1: bytes per block of kFmtThreads values (value + separator)
-__global__ void fmt_len_kernel(const double* __restrict__ v, int64_t count, unsigned long long* __restrict__ block_bytes) {
-  const int64_t i = (int64_t)blockIdx.x * kFmtThreads + threadIdx.x;
-  char buf[32];
-  unsigned len = 0;
-  if (i < count) len = (unsigned)format_value(v[i], buf) + 1;
-  for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
-  __shared__ unsigned s[kFmtThreads / 32];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = len;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long tot = 0;
-    for (int w = 0; w < kFmtThreads / 32; w++) tot += s[w];
-    block_bytes[blockIdx.x] = tot;
-  }
-}
+// One pass with a decoupled look-back: block b (ids taken in execution
+// order from a counter, so every predecessor is running or done) formats its
+// 256 values once into shared memory, publishes its byte count, sums its
+// predecessors' counts (stopping at the first inclusive prefix) and streams
+// its bytes to their final offset.  Status word: 2 flag bits (1 = block
+// total, 2 = inclusive prefix) over a 62-bit count.
+constexpr unsigned long long kFlagAgg = 1ULL << 62, kFlagIncl = 2ULL << 62, kValMask = (1ULL << 62) - 1;
 
-// pass 2: format into shared memory at the block-local offsets, then copy
-// the block's contiguous bytes to out + block offset
-__global__ void fmt_write_kernel(const double* __restrict__ v, int64_t count, int64_t cols,
-                                 const unsigned long long* __restrict__ block_offsets, unsigned char* __restrict__ out) {
-  __shared__ unsigned char stage[kFmtThreads * kFmtMax];
+__global__ void __launch_bounds__(kFmtThreads) fmt_kernel(const double* __restrict__ v, int64_t count, int64_t cols,
+                                                          unsigned char* __restrict__ out,
+                                                          unsigned long long* __restrict__ status,
+                                                          unsigned long long* __restrict__ counter,
+                                                          unsigned long long* __restrict__ nbytes, int64_t nblocks) {
+  __shared__ unsigned char stage[kFmtThreads * kFmtPer * kFmtMax];
   __shared__ unsigned ws[kFmtThreads / 32];
-  const int64_t i = (int64_t)blockIdx.x * kFmtThreads + threadIdx.x;
-  char buf[32];
+  __shared__ unsigned long long s_bid, s_off;
+  __shared__ int64_t s_col0;
+  if (threadIdx.x == 0) {
+    const unsigned long long bid = atomicAdd(counter, 1ULL);
+    s_bid = bid;
+    s_col0 = (int64_t)(bid * kFmtThreads * kFmtPer) % cols;
+  }
+  __syncthreads();
+  const unsigned long long bid = s_bid;
+  // kFmtPer consecutive values per thread
+  const int64_t i0 = ((int64_t)bid * kFmtThreads + threadIdx.x) * kFmtPer;
+  nc::Fmt f[kFmtPer];
+  unsigned lens[kFmtPer];
+  unsigned nl = 0;  // '\n' after value k <=> bit k
   unsigned len = 0;
-  if (i < count) {
-    len = (unsigned)format_value(v[i], buf);
-    buf[len] = (i % cols == cols - 1) ? '\n' : ' ';
-    len += 1;
+  int64_t col = (s_col0 + (int64_t)threadIdx.x * kFmtPer) % cols;
+#pragma unroll
+  for (int k = 0; k < kFmtPer; k++) {
+    lens[k] = 0;
+    if (i0 + k < count) {
+      f[k] = nc::nc_prepare(v[i0 + k], (const uint64_t(*)[2])kPow5Inv, (const uint64_t(*)[2])kPow5);
+      lens[k] = (unsigned)f[k].len + 1;
+      if (col == cols - 1) nl |= 1u << k;
+    }
+    col = col + 1 == cols ? 0 : col + 1;
+    len += lens[k];
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned x = len;
@@ -264,10 +289,52 @@ __global__ void fmt_write_kernel(const double* __restrict__ v, int64_t count, in
     if (w < warp) woff += ws[w];
     total += ws[w];
   }
-  const unsigned off = woff + x - len;
-  for (unsigned k = 0; k < len; k++) stage[off + k] = (unsigned char)buf[k];
+  if (warp == 0) {
+    // warp-parallel look-back: lane l inspects block j - l of a 32-block
+    // window; the window is consumed up to its nearest inclusive prefix once
+    // every status up to it is published
+    volatile unsigned long long* vs = status;
+    if (lane == 0) {
+      __threadfence();
+      vs[bid] = (bid == 0 ? kFlagIncl : kFlagAgg) | total;
+    }
+    unsigned long long prefix = 0;
+    long long j = (long long)bid - 1;
+    while (j >= 0) {
+      const long long jj = j - lane;
+      const unsigned long long st = jj >= 0 ? vs[jj] : (2ULL << 62);  // before block 0: an empty inclusive prefix
+      const unsigned ready = __ballot_sync(0xffffffffu, (st & ~kValMask) != 0);
+      const unsigned incl = __ballot_sync(0xffffffffu, (st & kFlagIncl) != 0);
+      const int first_incl = incl ? __ffs(incl) - 1 : 32;  // nearest inclusive in the window
+      const unsigned need = first_incl >= 31 ? 0xffffffffu : ((2u << first_incl) - 1u);
+      if ((ready & need) != need) continue;  // a predecessor in range has not published yet
+      unsigned long long add = (lane <= first_incl && jj >= 0) ? (st & kValMask) : 0;
+      for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+      prefix += add;
+      if (first_incl < 32) break;
+      j -= 32;
+    }
+    if (lane == 0) {
+      if (bid != 0) {
+        __threadfence();
+        vs[bid] = kFlagIncl | (prefix + total);
+      }
+      s_off = prefix;
+      if (bid == (unsigned long long)nblocks - 1) *nbytes = prefix + total;
+    }
+  }
   __syncthreads();
-  unsigned char* dst = out + block_offsets[blockIdx.x];
+  unsigned off = woff + x - len;
+#pragma unroll
+  for (int k = 0; k < kFmtPer; k++) {
+    if (lens[k]) {
+      nc::nc_emit(f[k], reinterpret_cast<char*>(stage) + off);  // straight into shared memory
+      stage[off + lens[k] - 1] = (nl >> k) & 1u ? '\n' : ' ';
+      off += lens[k];
+    }
+  }
+  __syncthreads();
+  unsigned char* dst = out + s_off;
   for (unsigned k = threadIdx.x; k < total; k += kFmtThreads) dst[k] = stage[k];
 }
 
@@ -324,31 +391,27 @@ size_t wg_ascii_format_scratch_bytes(int64_t count) {
   return 256 + (size_t)((count + kFmtThreads - 1) / kFmtThreads + 1) * 8;
 }
 
-int wg_ascii_format_size(const double* values, int64_t count, uint64_t* nbytes, void* scratch, void* stream) {
-  if (count < 0 || !nbytes || !scratch || (count > 0 && !values)) return wg::set_error(WG_EARG, "null buffer");
+int64_t wg_ascii_format_capacity(int64_t count) { return count < 0 ? -1 : count * kFmtMax; }
+
+int wg_ascii_format(const double* values, int64_t count, int64_t cols, uint8_t* out, int64_t cap, uint64_t* nbytes,
+                    void* scratch, void* stream) {
+  if (count < 0 || cols < 1 || !scratch || !nbytes || (count > 0 && (!values || !out)))
+    return wg::set_error(WG_EARG, "bad args");
+  if (cap < count * kFmtMax) return wg::set_error(WG_EARG, "capacity %lld < %lld", (long long)cap,
+                                                  (long long)(count * kFmtMax));
   cudaStream_t st = wg::as_stream(stream);
   if (count == 0) {
     WG_CUDA_TRY(cudaMemsetAsync(nbytes, 0, sizeof(uint64_t), st));
     return WG_OK;
   }
-  const int64_t blocks = (count + kFmtThreads - 1) / kFmtThreads;
+  const int64_t blocks = (count + kFmtThreads * kFmtPer - 1) / (kFmtThreads * kFmtPer);
   if (blocks > 0x7fffffff) return wg::set_error(WG_ELIMIT, "too many values");
-  unsigned long long* bb = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(scratch) + 256);
-  fmt_len_kernel<<<(unsigned)blocks, kFmtThreads, 0, st>>>(values, count, bb);
-  WG_LAUNCH_CHECK("fmt_len_kernel");
-  scan_kernel<<<1, 1024, 0, st>>>(bb, blocks, reinterpret_cast<unsigned long long*>(nbytes));
-  WG_LAUNCH_CHECK("scan_kernel");
-  return WG_OK;
-}
-
-int wg_ascii_format_write(const double* values, int64_t count, int64_t cols, uint8_t* out, void* scratch,
-                          void* stream) {
-  if (count < 0 || cols < 1 || !scratch || (count > 0 && (!values || !out))) return wg::set_error(WG_EARG, "bad args");
-  if (count == 0) return WG_OK;
-  const int64_t blocks = (count + kFmtThreads - 1) / kFmtThreads;
-  const unsigned long long* bb = reinterpret_cast<const unsigned long long*>(static_cast<unsigned char*>(scratch) + 256);
-  fmt_write_kernel<<<(unsigned)blocks, kFmtThreads, 0, wg::as_stream(stream)>>>(values, count, cols, bb, out);
-  WG_LAUNCH_CHECK("fmt_write_kernel");
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(scratch);
+  unsigned long long* status = counter + 32;  // 256-byte offset
+  WG_CUDA_TRY(cudaMemsetAsync(scratch, 0, 256 + (size_t)blocks * 8, st));
+  fmt_kernel<<<(unsigned)blocks, kFmtThreads, 0, st>>>(values, count, cols, out, status, counter,
+                                                     reinterpret_cast<unsigned long long*>(nbytes), blocks);
+  WG_LAUNCH_CHECK("fmt_kernel");
   return WG_OK;
 }
 

@@ -567,76 +567,141 @@ NC_HD void ryu_d2d(uint64_t ieee_m, uint32_t ieee_e, uint64_t& output, int32_t& 
   exp10 = e10 + removed;
 }
 
-NC_HD int write_uint(uint64_t v, char* buf) {  // decimal digits, returns length
-  char tmp[20];
-  int n = 0;
-  do {
-    const uint64_t q = v / 10;
-    tmp[n++] = (char)('0' + (v - 10 * q));
-    v = q;
-  } while (v != 0);
-  for (int i = 0; i < n; i++) buf[i] = tmp[n - 1 - i];
+NC_HD int decimal_length(uint64_t v) {  // digits of v (>= 1)
+  int n = 1;
+  while (v >= 10) {
+    v /= 10;
+    n++;
+  }
   return n;
+}
+
+// v's nd decimal digits into dst[0, nd), written from the right (no
+// temporary: dst may be shared memory)
+NC_HD void put_digits(uint64_t v, int nd, char* dst) {
+  for (int i = nd - 1; i >= 0; i--) {
+    const uint64_t q = v / 10;
+    dst[i] = (char)('0' + (v - 10 * q));
+    v = q;
+  }
+}
+
+// format_number(v) in two steps so a caller can place the text before
+// producing it: nc_prepare decides the form and its length, nc_emit writes
+// exactly that many characters.
+struct Fmt {
+  uint64_t m;   // integer value, or the shortest decimal significand
+  int32_t e10;  // repr: value = m * 10^e10
+  int nd;       // digits of m
+  int kind;     // 0 integer, 1 repr exponent form, 2 repr 0.000ddd, 3 repr ddd000.0, 4 repr ddd.ddd, 5 inf, 6 nan
+  bool neg;
+  int len;
+};
+
+NC_HD Fmt nc_prepare(double v, const uint64_t (*pow5inv)[2], const uint64_t (*pow5)[2]) {
+  Fmt f{};
+  const uint64_t bits = double_to_bits(v);
+  f.neg = (bits >> 63) != 0;
+  const uint32_t ieee_e = (uint32_t)((bits >> 52) & 0x7FF);
+  const uint64_t ieee_m = bits & ((1ULL << 52) - 1);
+  if (ieee_e == 0x7FF) {
+    f.kind = ieee_m != 0 ? 6 : 5;
+    f.len = ieee_m != 0 ? 3 : 3 + (f.neg ? 1 : 0);
+    return f;
+  }
+  const double a = f.neg ? -v : v;
+  if (a < 1e16 && a == (double)(int64_t)a) {  // integral: str(int(v)); -0.0 -> "0"
+    f.kind = 0;
+    f.m = (uint64_t)(int64_t)a;
+    f.nd = decimal_length(f.m);
+    f.neg = f.neg && f.m != 0;
+    f.len = f.nd + (f.neg ? 1 : 0);
+    return f;
+  }
+  ryu_d2d(ieee_m, ieee_e, f.m, f.e10, pow5inv, pow5);
+  f.nd = decimal_length(f.m);
+  const int decpt = f.nd + f.e10;
+  int n = f.neg ? 1 : 0;
+  if (decpt <= -4 || decpt > 16) {
+    f.kind = 1;
+    int x = decpt - 1;
+    if (x < 0) x = -x;
+    n += 1 + (f.nd > 1 ? f.nd : 0) + 2 + (x < 10 ? 2 : decimal_length((uint64_t)x));
+  } else if (decpt <= 0) {
+    f.kind = 2;
+    n += 2 + (-decpt) + f.nd;
+  } else if (decpt >= f.nd) {
+    f.kind = 3;
+    n += decpt + 2;
+  } else {
+    f.kind = 4;
+    n += f.nd + 1;
+  }
+  f.len = n;
+  return f;
+}
+
+NC_HD void nc_emit(const Fmt& f, char* dst) {
+  int n = 0;
+  if (f.kind == 6) {
+    dst[0] = 'n', dst[1] = 'a', dst[2] = 'n';
+    return;
+  }
+  if (f.neg) dst[n++] = '-';
+  if (f.kind == 5) {
+    dst[n++] = 'i', dst[n++] = 'n', dst[n++] = 'f';
+    return;
+  }
+  if (f.kind == 0) {
+    put_digits(f.m, f.nd, dst + n);
+    return;
+  }
+  const int nd = f.nd, decpt = nd + f.e10;
+  if (f.kind == 1) {
+    // d[.ddd]e[+-]xx
+    if (nd > 1) {
+      put_digits(f.m, nd, dst + n + 1);  // digits at n+1 .. n+nd, then move the first one left
+      dst[n] = dst[n + 1];
+      dst[n + 1] = '.';
+      n += nd + 1;
+    } else {
+      dst[n++] = (char)('0' + f.m);
+    }
+    dst[n++] = 'e';
+    int x = decpt - 1;
+    dst[n++] = x < 0 ? '-' : '+';
+    if (x < 0) x = -x;
+    if (x < 10) {
+      dst[n++] = '0';
+      dst[n++] = (char)('0' + x);
+    } else {
+      put_digits((uint64_t)x, decimal_length((uint64_t)x), dst + n);
+    }
+  } else if (f.kind == 2) {
+    dst[n++] = '0';
+    dst[n++] = '.';
+    for (int i = 0; i < -decpt; i++) dst[n++] = '0';
+    put_digits(f.m, nd, dst + n);
+  } else if (f.kind == 3) {
+    put_digits(f.m, nd, dst + n);
+    n += nd;
+    for (int i = nd; i < decpt; i++) dst[n++] = '0';
+    dst[n++] = '.';
+    dst[n++] = '0';
+  } else {
+    // ddd.ddd: digits at n .. n+nd, then open the point at decpt
+    put_digits(f.m / 1, nd, dst + n);  // all digits, shifted below
+    for (int i = nd; i > decpt; i--) dst[n + i] = dst[n + i - 1];
+    dst[n + decpt] = '.';
+  }
 }
 
 // format_number(v) (asciigrid.py:160-167) into buf (>= 25 bytes); returns
 // the length.  Non-finite values print as CPython's repr ('inf', 'nan').
 NC_HD int nc_format(double v, char* buf, const uint64_t (*pow5inv)[2], const uint64_t (*pow5)[2]) {
-  const uint64_t bits = double_to_bits(v);
-  const bool neg = (bits >> 63) != 0;
-  const uint32_t ieee_e = (uint32_t)((bits >> 52) & 0x7FF);
-  const uint64_t ieee_m = bits & ((1ULL << 52) - 1);
-  int n = 0;
-  if (ieee_e == 0x7FF) {
-    if (ieee_m != 0) {
-      buf[0] = 'n', buf[1] = 'a', buf[2] = 'n';
-      return 3;
-    }
-    if (neg) buf[n++] = '-';
-    buf[n++] = 'i', buf[n++] = 'n', buf[n++] = 'f';
-    return n;
-  }
-  const double a = neg ? -v : v;
-  if (a < 1e16 && a == (double)(int64_t)a) {  // integral: str(int(v)); -0.0 -> "0"
-    const uint64_t k = (uint64_t)(int64_t)a;
-    if (neg && k != 0) buf[n++] = '-';
-    return n + write_uint(k, buf + n);
-  }
-  if (neg) buf[n++] = '-';
-  uint64_t out;
-  int32_t e10;
-  ryu_d2d(ieee_m, ieee_e, out, e10, pow5inv, pow5);
-  char dig[20];
-  const int nd = write_uint(out, dig);
-  const int decpt = nd + e10;
-  if (decpt <= -4 || decpt > 16) {
-    buf[n++] = dig[0];
-    if (nd > 1) {
-      buf[n++] = '.';
-      for (int i = 1; i < nd; i++) buf[n++] = dig[i];
-    }
-    buf[n++] = 'e';
-    int x = decpt - 1;
-    buf[n++] = x < 0 ? '-' : '+';
-    if (x < 0) x = -x;
-    if (x < 10) buf[n++] = '0';
-    n += write_uint((uint64_t)x, buf + n);
-  } else if (decpt <= 0) {
-    buf[n++] = '0';
-    buf[n++] = '.';
-    for (int i = 0; i < -decpt; i++) buf[n++] = '0';
-    for (int i = 0; i < nd; i++) buf[n++] = dig[i];
-  } else if (decpt >= nd) {
-    for (int i = 0; i < nd; i++) buf[n++] = dig[i];
-    for (int i = nd; i < decpt; i++) buf[n++] = '0';
-    buf[n++] = '.';
-    buf[n++] = '0';
-  } else {
-    for (int i = 0; i < decpt; i++) buf[n++] = dig[i];
-    buf[n++] = '.';
-    for (int i = decpt; i < nd; i++) buf[n++] = dig[i];
-  }
-  return n;
+  const Fmt f = nc_prepare(v, pow5inv, pow5);
+  nc_emit(f, buf);
+  return f.len;
 }
 
 }  // namespace nc

@@ -43,20 +43,20 @@ def main():
     v = g.device_elevations().view(-1)
     scratch = _device.empty((int(L.wg_ascii_format_scratch_bytes(count)),), torch.uint8)
     nb = _device.empty((1,), torch.int64)
-    L.wg_ascii_format_size(_lib.ptr(v), count, _lib.ptr(nb), _lib.ptr(scratch), _lib.stream_ptr())
-    nbytes = int(_device.read_small(nb)[0])
-    body = _device.empty((nbytes,), torch.uint8)
+    cap = int(L.wg_ascii_format_capacity(count))
+    body = _device.empty((cap,), torch.uint8)
     wt = []
     for _ in range(a.reps + 1):
         e0, e1 = events()
         e0.record()
-        L.wg_ascii_format_size(_lib.ptr(v), count, _lib.ptr(nb), _lib.ptr(scratch), _lib.stream_ptr())
-        L.wg_ascii_format_write(_lib.ptr(v), count, n, _lib.ptr(body), _lib.ptr(scratch), _lib.stream_ptr())
+        L.wg_ascii_format(_lib.ptr(v), count, n, _lib.ptr(body), cap, _lib.ptr(nb), _lib.ptr(scratch),
+                          _lib.stream_ptr())
         e1.record()
         torch.cuda.synchronize()
         wt.append(e0.elapsed_time(e1))
     write_ms = min(wt[1:])
-    del scratch
+    nbytes = int(_device.read_small(nb)[0])
+    del scratch, body
 
     # ---- writer end to end: DemGrid -> bytes on the host
     t0 = time.perf_counter()
