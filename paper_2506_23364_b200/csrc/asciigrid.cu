@@ -182,35 +182,16 @@ __device__ __forceinline__ bool parse_fast(const unsigned char* __restrict__ t, 
   if (wsm == 0) return false;  // token of 24+ bytes
   const int len = __ffs(wsm) - 1;
   *len_out = len;
-  const unsigned c0 = w[0] & 255u;
-  const bool neg = c0 == '-';
-  const int k0 = (c0 == '-' || c0 == '+') ? 1 : 0;
-  uint64_t m = 0;
-  int kept = 0, frac = 0;
-  bool dot = false, any = false, bad = false;
+  // the token's bytes as three little-endian words (+ a zero word)
+  uint64_t W[4];
 #pragma unroll
-  for (int k = 0; k < 24; k++) {  // fully unrolled: the bytes stay in registers
-    if (k >= k0 && k < len) {
-      const unsigned c = (w[k >> 2] >> (8 * (k & 3))) & 255u;
-      const unsigned d = c - '0';
-      if (d <= 9) {
-        any = true;
-        if (m != 0 || d != 0) {
-          bad |= kept == 19;
-          m = m * 10 + d;
-          kept++;
-        }
-        frac += dot ? 1 : 0;
-      } else {
-        bad |= !(c == '.' && !dot);
-        dot = true;
-      }
-    }
+  for (int k = 0; k < 3; k++) {
+    const int b0 = 8 * k;  // bytes beyond the token are masked to 0 below
+    W[k] = (uint64_t)w[2 * k] | ((uint64_t)w[2 * k + 1] << 32);
+    if (len < b0 + 8) W[k] &= len <= b0 ? 0ULL : (~0ULL >> (64 - 8 * (len - b0)));
   }
-  if (bad || !any) return false;
-  const uint64_t bits = m == 0 ? 0 : nc::el_convert(-(int64_t)frac, m, (const uint64_t(*)[2])kEL);
-  *v = nc::bits_to_double(bits | (neg ? 0x8000000000000000ULL : 0));
-  return true;
+  W[3] = 0;
+  return nc::nc_parse_simple(W, len, v, (const uint64_t(*)[2])kEL);
 }
 
 __global__ void parse_kernel(const unsigned char* __restrict__ t, int64_t n, const int64_t* __restrict__ starts,

@@ -419,6 +419,96 @@ NC_HD int nc_parse(const unsigned char* s, int n, double* out, const uint64_t (*
   return 0;
 }
 
+// ---- SWAR fast path for plain numerals --------------------------------------
+// [+-]digits[.digits] with <= 19 digits in all, no exponent or underscore: the
+// token's (<= 24) bytes arrive as three little-endian words; digit runs are
+// validated and converted eight at a time (Lemire's eight-digit trick) and
+// the value goes through the same Eisel-Lemire step as nc_parse.  Returns
+// false for any other shape (the caller then runs nc_parse).
+
+NC_HD int ctz64(uint64_t x) {
+#ifdef __CUDA_ARCH__
+  return __ffsll((long long)x) - 1;
+#else
+  return __builtin_ctzll(x);
+#endif
+}
+
+// bytes [off, off + 8) of the 24-byte token (W[3] must be 0), off in [-8, 16];
+// bytes before 0 read as '0'
+NC_HD uint64_t bytes8(const uint64_t* W, int off) {
+  if (off < 0) {
+    const int k = -off;  // 1..8 leading fill bytes
+    const uint64_t x = k >= 8 ? 0 : (W[0] << (8 * k));
+    const uint64_t fill = k >= 8 ? ~0ULL : ((1ULL << (8 * k)) - 1);
+    return x | (0x3030303030303030ULL & fill);
+  }
+  const int q = off >> 3, r = off & 7;
+  return r == 0 ? W[q] : (W[q] >> (8 * r)) | (W[q + 1] << (64 - 8 * r));
+}
+
+NC_HD bool eight_digits(uint64_t x) {
+  return (((x + 0x4646464646464646ULL) | (x - 0x3030303030303030ULL)) & 0x8080808080808080ULL) == 0;
+}
+
+NC_HD uint64_t parse8(uint64_t x) {
+  x = (x & 0x0F0F0F0F0F0F0F0FULL) * 2561 >> 8;
+  x = (x & 0x00FF00FF00FF00FFULL) * 6553601 >> 16;
+  return (x & 0x0000FFFF0000FFFFULL) * 42949672960001ULL >> 32;
+}
+
+// digits [a, a + n) (0 <= n <= 8) right-aligned: bytes before the run read '0'
+NC_HD bool digits8(const uint64_t* W, int a, int n, uint64_t& v) {
+  uint64_t x = bytes8(W, a + n - 8);
+  const int k = 8 - n;
+  if (k > 0) {
+    const uint64_t fill = k >= 8 ? ~0ULL : ((1ULL << (8 * k)) - 1);
+    x = (x & ~fill) | (0x3030303030303030ULL & fill);
+  }
+  if (!eight_digits(x)) return false;
+  v = parse8(x);
+  return true;
+}
+
+// digits [a, a + n) (0 <= n <= 16) as an integer; false if a byte is not a
+// digit (no recursion: device stacks are sized statically)
+NC_HD bool digits_value(const uint64_t* W, int a, int n, uint64_t& v) {
+  v = 0;
+  if (n == 0) return true;
+  if (n <= 8) return digits8(W, a, n, v);
+  uint64_t hi, lo;
+  if (!digits8(W, a, n - 8, hi) || !digits8(W, a + n - 8, 8, lo)) return false;
+  v = hi * 100000000ULL + lo;
+  return true;
+}
+
+NC_HD bool nc_parse_simple(const uint64_t* W, int len, double* out, const uint64_t (*tab)[2]) {
+  if (len < 1 || len > 24) return false;
+  const unsigned c0 = (unsigned)(W[0] & 255u);
+  const int s0 = (c0 == '-' || c0 == '+') ? 1 : 0;
+  // first '.' (zero-byte test on W ^ '.')
+  int p = len;
+  for (int q = 0; q < 3; q++) {
+    const uint64_t t = W[q] ^ 0x2E2E2E2E2E2E2E2EULL;
+    const uint64_t z = (t - 0x0101010101010101ULL) & ~t & 0x8080808080808080ULL;
+    if (z) {
+      const int pos = 8 * q + (ctz64(z) >> 3);
+      if (pos < len) p = pos;
+      break;
+    }
+  }
+  const int ni = p - s0, nf = p < len ? len - p - 1 : 0;
+  if (ni < 0 || ni + nf < 1 || ni > 16 || nf > 16 || ni + nf > 19) return false;
+  uint64_t iv, fv;
+  if (!digits_value(W, s0, ni, iv) || !digits_value(W, p + 1, nf, fv)) return false;
+  uint64_t scale = 1;
+  for (int k = 0; k < nf; k++) scale *= 10;
+  const uint64_t m = iv * scale + fv;
+  const uint64_t bits = m == 0 ? 0 : el_convert(-(int64_t)nf, m, tab);
+  *out = bits_to_double(bits | (c0 == '-' ? 0x8000000000000000ULL : 0));
+  return true;
+}
+
 // ---- formatting ----------------------------------------------------------
 
 NC_HD uint32_t pow5bits(int32_t e) { return (uint32_t)(((uint32_t)e * 1217359) >> 19) + 1; }

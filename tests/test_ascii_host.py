@@ -61,6 +61,14 @@ def test_numconv_host_build_matches_cpython():
     for t, g, s in zip(toks, got, st):
         w, ws = check.ref_parse(t)
         assert ws == s and (s != 0 or check.same(w, g)), t
+    # the SWAR fast path (plain numerals): whenever it takes a token, float()'s value
+    reprs = [repr(float(v)) for v in np.random.default_rng(7).uniform(-5e3, 5e3, 20_000)]
+    simple, sst = check.parse_simple_many(lib, toks + reprs)
+    assert sst.sum() > 20_000
+    for t, g, s in zip(toks + reprs, simple, sst):
+        if s:
+            w, ws = check.ref_parse(t)
+            assert ws == 0 and check.same(w, g), t
     bits = np.random.default_rng(5).integers(0, 2**64, size=60_000, dtype=np.uint64).view(np.float64)
     vals = np.concatenate([bits[np.isfinite(bits)], np.round(np.random.default_rng(6).uniform(-500, 4800, 20_000), 2)])
     for v, s in zip(vals, check.format_many(lib, vals)):

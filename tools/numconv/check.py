@@ -26,6 +26,7 @@ def build():
     lib.nc_parse_many.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                   ctypes.c_void_p, ctypes.c_void_p]
     lib.nc_format_many.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.nc_parse_simple_many.argtypes = lib.nc_parse_many.argtypes
     return lib
 
 
@@ -44,6 +45,17 @@ def parse_many(lib, toks):
     out = np.zeros(len(toks), dtype=np.float64)
     st = np.zeros(len(toks), dtype=np.int32)
     lib.nc_parse_many(data, offs.ctypes.data, lens.ctypes.data, len(toks), out.ctypes.data, st.ctypes.data)
+    return out, st
+
+
+def parse_simple_many(lib, toks):
+    data = "".join(toks).encode("ascii")
+    lens = np.array([len(t) for t in toks], dtype=np.int32)
+    offs = np.zeros(len(toks), dtype=np.int64)
+    offs[1:] = np.cumsum(lens[:-1])
+    out = np.zeros(len(toks), dtype=np.float64)
+    st = np.zeros(len(toks), dtype=np.int32)
+    lib.nc_parse_simple_many(data, offs.ctypes.data, lens.ctypes.data, len(toks), out.ctypes.data, st.ctypes.data)
     return out, st
 
 
@@ -129,6 +141,7 @@ def main():
             bad += 1
             if bad < 10:
                 print("FORMAT", repr(v), g, want)
+    got_reprs = list(got)
     back, st = parse_many(lib, got)
     # format_number drops the sign of -0.0 (str(int(-0.0)) == "0"), like the reference
     mism = np.nonzero(((back.view(np.int64) != allv.view(np.int64)) & ~((allv == 0) & (back == 0))) | (st != 0))[0]
@@ -154,6 +167,18 @@ def main():
                 print("PARSE", repr(t), g, s, "want", w, ws)
         n_fast += 1
     print(f"parse: {n_fast} tokens checked")
+    # the SWAR fast path: whenever it handles a token, the value is float()'s
+    got2, st2 = parse_simple_many(lib, toks + got_reprs)
+    handled = 0
+    for t, g, s in zip(toks + got_reprs, got2, st2):
+        if s:
+            handled += 1
+            w, ws = ref_parse(t)
+            if ws != 0 or not same(w, g):
+                bad += 1
+                if bad < 30:
+                    print("SIMPLE", repr(t), g, "want", w, ws)
+    print(f"fast path: {handled} tokens handled")
     print("MISMATCHES", bad)
     sys.exit(1 if bad else 0)
 
