@@ -61,17 +61,6 @@ __device__ __forceinline__ unsigned filt(int type, unsigned x, unsigned a, unsig
 
 __device__ __forceinline__ uint32_t rev(uint32_t v, int n) { return __brev(v) >> (32 - n); }
 
-// fixed-Huffman literal: (bits reversed for LSB-first packing, length)
-__device__ __forceinline__ void lit_code(unsigned lit, uint32_t& code, int& len) {
-  if (lit < 144) {
-    code = rev(0x30 + lit, 8);
-    len = 8;
-  } else {
-    code = rev(0x190 + (lit - 144), 9);
-    len = 9;
-  }
-}
-
 // Bit sink: count (kWrite false) or OR into the zeroed stream at bit offset.
 template <bool kWrite>
 struct Bits {
@@ -227,75 +216,6 @@ __device__ uint32_t warp_crc32(const uint8_t* p, int64_t n, const uint32_t* tabl
       if (s_len[l] > 0) crc = multmodp(x8nmodp((uint64_t)s_len[l]), crc) ^ s_crc[l];
   }
   return __shfl_sync(0xffffffffu, crc, 0);
-}
-
-
-// fixed-Huffman length symbol for L (3..258): reversed code | extra << n, bits
-__device__ __forceinline__ void len_code(unsigned L, uint32_t& code, int& len) {
-  unsigned sym, extra = 0, ebits = 0;
-  if (L == 258) {
-    sym = 285;
-  } else if (L <= 10) {
-    sym = 254 + L;
-  } else {
-    const unsigned l = L - 3;  // 8..254
-    const int eb = 31 - __clz(l) - 2;  // extra bits (1..5)
-    sym = 265 + (eb - 1) * 4 + ((l >> eb) - 4);
-    extra = l & ((1u << eb) - 1);
-    ebits = eb;
-  }
-  int n;
-  uint32_t c;
-  if (sym < 280) {
-    c = rev(sym - 256, 7);
-    n = 7;
-  } else {
-    c = rev(0xC0 + (sym - 280), 8);
-    n = 8;
-  }
-  code = c | (extra << n);
-  len = n + (int)ebits;
-}
-
-// fixed distance code (5 bits, reversed) + extra bits for d in 1..32768
-__device__ __forceinline__ void dist_code(unsigned d, uint32_t& code, int& len) {
-  unsigned sym, extra = 0;
-  int eb = 0;
-  if (d <= 4) {
-    sym = d - 1;
-  } else {
-    const unsigned l = d - 1;
-    eb = 31 - __clz(l) - 1;
-    sym = 2 * (eb + 1) + ((l >> eb) & 1);
-    extra = l & ((1u << eb) - 1);
-  }
-  code = rev(sym, 5) | (extra << 5);
-  len = 5 + eb;
-}
-
-// token: literal byte b (< 256), or match (L << 16) | (d - 1) with L >= 3
-__device__ __forceinline__ int token_bits(uint32_t t) {
-  if (t < 256) return t < 144 ? 8 : 9;
-  uint32_t c;
-  int a, b;
-  len_code(t >> 16, c, a);
-  dist_code((t & 0xFFFF) + 1, c, b);
-  return a + b;
-}
-
-template <bool kWrite>
-__device__ __forceinline__ void put_token(Bits<kWrite>& o, uint32_t t) {
-  uint32_t c;
-  int n;
-  if (t < 256) {
-    lit_code(t, c, n);
-    o.put(c, n);
-  } else {
-    len_code(t >> 16, c, n);
-    o.put(c, n);
-    dist_code((t & 0xFFFF) + 1, c, n);
-    o.put(c, n);
-  }
 }
 
 // Per-image scratch layout (wg_png_scratch_bytes).
