@@ -211,9 +211,6 @@ __global__ void parse_kernel(const unsigned char* __restrict__ t, int64_t n, con
   }
 }
 
-__device__ __forceinline__ int format_value(double v, char* buf) {
-  return nc::nc_format(v, buf, (const uint64_t(*)[2])kPow5Inv, (const uint64_t(*)[2])kPow5);
-}
 
 // One pass with a decoupled look-back: block b (ids taken in execution
 // order from a counter, so every predecessor is running or done) formats its
