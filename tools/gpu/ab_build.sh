@@ -1,9 +1,10 @@
 # A/B of trajectory-kernel compile variants (NVCC_EXTRA) with the in-process
+# (a variant may hold several flags separated by commas)
 # probe (REPS launches each; min and median ms), two interleaved rounds
 for round in 1 2; do
 for v in ${BUILDS:-"-DWG_TRAJ_MINBLOCKS=7"}; do
   make -C paper_2506_23364_b200/csrc clean >/dev/null
-  make -C paper_2506_23364_b200/csrc -j8 NVCC_EXTRA="$v" >/dev/null 2>&1 || { echo "build $v failed"; continue; }
+  make -C paper_2506_23364_b200/csrc -j8 NVCC_EXTRA="${v//,/ }" >/dev/null 2>&1 || { echo "build $v failed"; continue; }
   timeout 600 python tools/traj_probe.py --reps ${REPS:-6} > gpurun_out/ab.log 2>gpurun_out/ab.err
   echo "$round $v $(python -c "
 import json,statistics as st
