@@ -3,75 +3,117 @@
 // .tobytes(), workflow.py:465-529, which runs at ~0.33 GiB/s and dominated
 // cold and warm latency at scale -- SURVEY.md 0.7 / 8(f) rank 1).
 //
-// 256-bit result = four independent 64-bit lanes.  The payload is cut into
-// 256-byte chunks; each chunk is folded by a SplitMix-style nonlinear absorb
-// with its chunk index mixed in, and the four lane values of all chunks are
-// summed mod 2^64.  The sum is commutative, so the digest is independent of
-// launch geometry and thread scheduling, while the index mixing keeps it
-// position-sensitive.  SPEC.md:444 asks only for a stable hash of >= 128 bits;
-// the executor feeds these 32 bytes (plus type tags and headers) into a host
-// SHA-256 to form the 64-hex cache keys.
+// Definition.  A payload is `rows` rows of `row_bytes` bytes (row r at
+// data + r*ld).  Each row is read as little-endian 8-byte words (the last one
+// zero-padded), W = ceil(row_bytes / 8) per row, grouped in tiles of 1024
+// words; word w of tile t belongs to chunk (t, w mod 32) -- i.e. lane l of a
+// warp owns words l, l+32, ..., l+992 of the tile, so every load instruction
+// of a warp reads 256 contiguous bytes.  Chunk id c = (r*T + t)*32 + l
+// (T = tiles per row).  Each chunk absorbs its words in order into a 128-bit
+// state seeded with c (State below), and the four output words are sums
+// mod 2^64 over all chunks of finalised combinations of the state.  The sums are commutative, so the
+// digest is independent of launch geometry and scheduling, while the chunk
+// id keeps it position-sensitive; a strided window hashes exactly like the
+// same rows stored contiguously, and unaligned rows take a byte-assembling
+// path with the same words.  SPEC.md:444 asks only for a stable hash of
+// >= 128 bits; the executor feeds these 32 bytes (plus type tags and
+// headers) into a host SHA-256 to form the 64-hex cache keys.
 #include "wg_internal.cuh"
 
 namespace {
 
-__device__ const unsigned long long kSeeds[4] = {0x243F6A8885A308D3ULL, 0x13198A2E03707344ULL, 0xA4093822299F31D0ULL,
-                                          0x082EFA98EC4E6C89ULL};
 constexpr unsigned long long kGolden = 0x9E3779B97F4A7C15ULL;
+constexpr unsigned long long kSeedA = 0x243F6A8885A308D3ULL, kSeedB = 0x13198A2E03707344ULL;
+constexpr int kTileWords = 1024;
+#ifndef WG_DIGEST_UNROLL
+#define WG_DIGEST_UNROLL 32
+#endif
+constexpr int kUnroll = WG_DIGEST_UNROLL;  // loads in flight per lane
 
-__device__ __forceinline__ unsigned long long mix(unsigned long long x) {
+__device__ __forceinline__ unsigned long long mix_a(unsigned long long x) {  // SplitMix64 finaliser
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
   x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
   return x ^ (x >> 31);
 }
 
-// One pass over `rows` rows of `row_bytes` bytes each, row r starting at
-// data + r*ld: chunk (r, c) is the c-th 256-byte piece of row r and is mixed
-// with its global index r*cpr + c (cpr = chunks per row), so a strided window
-// hashes exactly like the same rows stored contiguously.
+__device__ __forceinline__ unsigned long long mix_b(unsigned long long x) {  // Moremur finaliser
+  x = (x ^ (x >> 27)) * 0x3C79AC492BA7B653ULL;
+  x = (x ^ (x >> 33)) * 0x1C69B3F74AC4AE35ULL;
+  return x ^ (x >> 27);
+}
+
+// 128-bit chunk state: a absorbs each word through the SplitMix64 bijection;
+// b folds in every intermediate a by an odd multiply (also a bijection), so
+// two equal-length word sequences collide only if both the final a and the
+// b chain do.  One finaliser per word keeps the kernel at HBM speed.
+struct State {
+  unsigned long long a, b;
+  __device__ __forceinline__ void absorb(unsigned long long v) {
+    a = mix_a(a ^ v);
+    b = (b ^ a) * 0xD6E8FEB86659FD93ULL;
+  }
+};
+
+// word w (< W) of a row that is not 8-byte aligned or ends mid-word
+__device__ __forceinline__ unsigned long long word_bytes(const unsigned char* row, int64_t w, int64_t row_bytes) {
+  unsigned long long x = 0;
+  const int64_t i0 = 8 * w;
+  const int n = (int)min((int64_t)8, row_bytes - i0);
+  for (int k = 0; k < n; k++) x |= (unsigned long long)__ldg(row + i0 + k) << (8 * k);
+  return x;
+}
+
 __global__ void digest_kernel(const unsigned char* __restrict__ data, int64_t rows, int64_t row_bytes, int64_t ld,
                               unsigned long long* __restrict__ out) {
-  const int64_t cpr = (row_bytes + 255) / 256;
-  const int64_t nchunks = rows * cpr;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (row_bytes + 7) >> 3;     // words per row
+  const int64_t Wfull = row_bytes >> 3;       // complete words per row
+  const int64_t T = (W + kTileWords - 1) / kTileWords;
+  const int64_t ntasks = rows * T;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long acc[4] = {0, 0, 0, 0};
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks; c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = c / cpr, k = c - r * cpr;
+  for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < ntasks; task += nwarps) {
+    const int64_t r = task / T, t = task - r * T;
     const unsigned char* row = data + r * ld;
-    const int64_t nbytes = row_bytes;
-    unsigned long long h[4];
-#pragma unroll
-    for (int l = 0; l < 4; l++) h[l] = mix(kSeeds[l] ^ ((unsigned long long)c * kGolden));
-    const int64_t base = k * 256;
-    const bool full = base + 256 <= nbytes && ((((uintptr_t)(row + base)) & 15) == 0);
-    if (full) {
-      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(row + base);
-#pragma unroll 4
-      for (int q = 0; q < 16; q++) {
-        const ulonglong2 v = __ldg(p + q);
-        h[q & 3] = mix(h[q & 3] ^ v.x) + v.y;
-        h[(q + 1) & 3] ^= mix(v.y + kGolden * (unsigned long long)(q + 1));
+    const unsigned long long c = (unsigned long long)task * 32 + lane;
+    State s{mix_a(kSeedA ^ (c * kGolden)), mix_b(kSeedB ^ (c * kGolden))};
+    const int64_t w0 = t * kTileWords + lane;
+    const bool aligned = (((uintptr_t)row) & 7) == 0;
+    if (aligned && (t + 1) * kTileWords <= Wfull) {
+      const unsigned long long* p = reinterpret_cast<const unsigned long long*>(row) + w0;
+#pragma unroll kUnroll
+      for (int j = 0; j < kTileWords / 32; j++) s.absorb(__ldg(p + 32 * j));
+    } else if (aligned && Wfull > 0) {  // the row's last, partial tile
+      const unsigned long long* p = reinterpret_cast<const unsigned long long*>(row);
+#pragma unroll kUnroll
+      for (int j = 0; j < kTileWords / 32; j++) {
+        const int64_t w = w0 + 32 * j;
+        // clamped address and a select instead of a branch: the loads of
+        // the unrolled iterations issue together, as in the full-tile loop
+        const unsigned long long v = __ldg(p + min(w, Wfull - 1));
+        State n = s;
+        n.absorb(v);
+        if (w < Wfull) s = n;
       }
-    } else {
-      // ragged or unaligned chunk: byte-wise little-endian words, zero padded
-      for (int q = 0; q < 16; q++) {
-        unsigned long long x = 0, y = 0;
-        for (int b = 0; b < 8; b++) {
-          const int64_t i0 = base + 16 * q + b, i1 = i0 + 8;
-          if (i0 < nbytes) x |= (unsigned long long)row[i0] << (8 * b);
-          if (i1 < nbytes) y |= (unsigned long long)row[i1] << (8 * b);
-        }
-        h[q & 3] = mix(h[q & 3] ^ x) + y;
-        h[(q + 1) & 3] ^= mix(y + kGolden * (unsigned long long)(q + 1));
+      // a ragged final word (row_bytes % 8 != 0) is the last of its lane
+      if (Wfull < W && ((Wfull - w0) & 31) == 0 && Wfull >= w0) s.absorb(word_bytes(row, Wfull, row_bytes));
+    } else {  // rows not 8-byte aligned
+      for (int j = 0; j < kTileWords / 32; j++) {
+        const int64_t w = w0 + 32 * j;
+        if (w >= W) break;
+        s.absorb(word_bytes(row, w, row_bytes));
       }
     }
-#pragma unroll
-    for (int l = 0; l < 4; l++) acc[l] += mix(h[l] + (unsigned long long)l);
+    acc[0] += mix_a(s.a + 0x5851F42D4C957F2DULL);
+    acc[1] += mix_b(s.b + 0x14057B7EF767814FULL);
+    acc[2] += mix_a(s.a ^ mix_b(s.b));
+    acc[3] += mix_b(s.b ^ mix_a(s.a + kGolden));
   }
 #pragma unroll
   for (int l = 0; l < 4; l++) {
     unsigned long long v = acc[l];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + l, v);
+    if (lane == 0 && v) atomicAdd(out + l, v);
   }
 }
 
@@ -82,8 +124,9 @@ extern "C" int wg_digest2d(const void* data, int64_t rows, int64_t row_bytes, in
   if (!out) return wg::set_error(WG_EARG, "null digest buffer");
   if (rows <= 0 || row_bytes <= 0) return WG_OK;
   if (!data || ld_bytes < row_bytes) return wg::set_error(WG_EARG, "bad digest arguments");
-  const int64_t nchunks = rows * ((row_bytes + 255) / 256);
-  digest_kernel<<<wg::stream_grid(nchunks, 256, 4), 256, 0, wg::as_stream(stream)>>>(
+  const int64_t W = (row_bytes + 7) / 8;
+  const int64_t nthreads = rows * ((W + kTileWords - 1) / kTileWords) * 32;  // one warp per tile
+  digest_kernel<<<wg::stream_grid(nthreads, 256, 8), 256, 0, wg::as_stream(stream)>>>(
       reinterpret_cast<const unsigned char*>(data), rows, row_bytes, ld_bytes,
       reinterpret_cast<unsigned long long*>(out));
   WG_LAUNCH_CHECK("digest_kernel");
