@@ -216,13 +216,10 @@ def write_ascii_grid_bytes(grid: DemGrid) -> memoryview:
                                  _lib.ptr(scratch), _lib.stream_ptr()))
     nbytes = int(_device.read_small(nb)[0])
     out = full[: len(head) + nbytes]
-    # one pageable D2H straight into uninitialised host memory: at multi-GB
-    # sizes first-touch page zeroing (~5 GB/s) bounds any strategy, and
-    # bytearray's zero-fill or pinned staging only add to it
-    # (tools/d2h_probe.py)
-    buf = np.empty(out.numel(), dtype=np.uint8)
-    if buf.size:
-        torch.from_numpy(buf).copy_(out)
+    # staged through pinned chunks by a thread pool (_device.download): a
+    # single pageable copy into fresh host memory is bound by first-touch
+    # page faults at multi-GB sizes (tools/host_xfer_probe.py)
+    buf = _device.download(out)
     return memoryview(buf)
 
 

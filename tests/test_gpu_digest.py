@@ -109,3 +109,31 @@ def test_digest_content_addressing():
     # deterministic across launches and a large payload (several tiles per row)
     x = torch.arange(1 << 22, dtype=torch.int64, device="cuda")
     assert device_digest(x) == device_digest(x.clone())
+
+
+# -- staged host transfers (_device.upload / download above 64 MiB) ---------
+
+
+@pytest.mark.parametrize("dtype,shape", [(torch.uint8, ((64 << 20) + 13,)), (torch.float64, (3001, 4099)),
+                                         (torch.bool, ((200 << 20) + 7,)), (torch.int64, (9, 1 << 20, 1))])
+def test_staged_transfers_round_trip(dtype, shape):
+    from paper_2506_23364_b200 import _device
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n = int(np.prod(shape))
+    raw = torch.randint(0, 256, (n * torch.empty(0, dtype=dtype).element_size(),), dtype=torch.uint8,
+                        device="cuda", generator=g)
+    if dtype == torch.bool:
+        raw = raw & 1
+    t = raw.view(dtype).view(shape)
+    t = t * 1 if dtype != torch.bool else t.clone()  # produced by a kernel just queued on the current stream
+    h = _device.download(t)
+    assert h.shape == tuple(shape) and h.flags.writeable
+    want = t.cpu().numpy()
+    assert np.array_equal(h.view(np.uint8), want.view(np.uint8))
+    v = _device.host_view(t)
+    assert not v.flags.writeable and np.array_equal(v.view(np.uint8), want.view(np.uint8))
+    back = _device.upload(h)
+    assert back.dtype == dtype and torch.equal(back.view(torch.uint8), t.view(torch.uint8))
+    ro = np.frombuffer(h.tobytes(), dtype=h.dtype).reshape(h.shape)  # read-only source
+    assert torch.equal(_device.upload(ro).view(torch.uint8), t.view(torch.uint8))

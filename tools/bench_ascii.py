@@ -59,9 +59,13 @@ def main():
     del scratch, body
 
     # ---- writer end to end: DemGrid -> bytes on the host
-    t0 = time.perf_counter()
-    doc = asciigrid.write_ascii_grid_bytes(g)
-    write_e2e_ms = (time.perf_counter() - t0) * 1e3
+    # (first call: includes the one-time pinned staging ring of _device)
+    we = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        doc = asciigrid.write_ascii_grid_bytes(g)
+        we.append((time.perf_counter() - t0) * 1e3)
+    write_e2e_first_ms, write_e2e_ms = we[0], min(we)
 
     # ---- reader: kernels only (text resident on the device)
     head_len = len(doc) - nbytes
@@ -88,10 +92,13 @@ def main():
     del t, starts, sc, vals
 
     # ---- reader end to end: host bytes -> DemGrid (incl. H2D + validation)
-    t0 = time.perf_counter()
-    h = asciigrid.parse_ascii_grid(doc)
-    torch.cuda.synchronize()
-    parse_e2e_ms = (time.perf_counter() - t0) * 1e3
+    pe = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        h = asciigrid.parse_ascii_grid(doc)
+        torch.cuda.synchronize()
+        pe.append((time.perf_counter() - t0) * 1e3)
+    parse_e2e_ms = min(pe)
     assert torch.equal(h.device_elevations().view(-1).view(torch.int64), v.view(torch.int64))
 
     # ---- CPU baseline: the reference algorithm on a sample, host cores
@@ -122,6 +129,7 @@ def main():
                                "bytes_per_unit": parse_bytes / count}},
         "write": {"kernel_ms": write_ms, "value": count / (write_ms / 1e3), "e2e_ms": write_e2e_ms,
                   "e2e_value": count / (write_e2e_ms / 1e3),
+                  "e2e_first_call_ms": write_e2e_first_ms,
                   "roofline": {"bound": "hbm", "achieved": write_bytes / (write_ms / 1e3) / 1e9, "peak": peak,
                                "unit": "GB/s", "frac": write_bytes / (write_ms / 1e3) / 1e9 / peak,
                                "bytes_per_unit": write_bytes / count}},
