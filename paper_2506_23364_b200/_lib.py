@@ -80,9 +80,8 @@ SIGNATURES: dict[str, tuple] = {
     "wg_png_scratch_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "wg_png_tiles": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_png_encode": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
-    "wg_ascii_tokenize_scratch_bytes": (c_size, [c_i64]),
-    "wg_ascii_tokenize": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
-    "wg_ascii_parse": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
+    "wg_ascii_read_scratch_bytes": (c_size, [c_i64, c_i64]),
+    "wg_ascii_read": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_ascii_format_scratch_bytes": (c_size, [c_i64]),
     "wg_ascii_format_capacity": (c_i64, [c_i64]),
     "wg_ascii_format": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),

@@ -160,36 +160,29 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
     dev = _device.device()
     n = len(data)
     t = _device.upload(np.frombuffer(data, dtype=np.uint8))
-    starts = torch.empty(expected + 1, dtype=torch.int64, device=dev)
-    cf = torch.empty(2, dtype=torch.int64, device=dev)
-    scratch = torch.empty(int(L.wg_ascii_tokenize_scratch_bytes(n)), dtype=torch.uint8, device=dev)
-    _lib.check(L.wg_ascii_tokenize(_lib.ptr(t), n, body_off, _lib.ptr(starts), expected + 1, _lib.ptr(cf),
-                                   _lib.ptr(scratch), _lib.stream_ptr()), AsciiGridError)
-    found, nonascii = _device.read_small(cf)
+    values = torch.empty(expected, dtype=torch.float64, device=dev)
+    info = torch.empty(4, dtype=torch.int64, device=dev)
+    scratch = torch.empty(int(L.wg_ascii_read_scratch_bytes(n, expected)), dtype=torch.uint8, device=dev)
+    _lib.check(L.wg_ascii_read(_lib.ptr(t), n, body_off, _lib.ptr(values), expected, _lib.ptr(info),
+                               _lib.ptr(scratch), _lib.stream_ptr()), AsciiGridError)
+    found, nonascii, extra_off, bad_off = (v & _NO_BAD for v in _device.read_small(info))
     if nonascii:
         raise AsciiGridError("document is not ASCII")
     if found != expected:
         if found < expected:
             raise AsciiGridError(f"expected {expected} elevation values, found {found}",
                                  line=_count_lines(full()))
-        off = int(_device.read_small(starts[expected:expected + 1])[0])
-        line, col = _line_col(full(), off)
+        line, col = _line_col(full(), extra_off)
         raise AsciiGridError(f"expected {expected} elevation values, found {found}", line=line, column=col)
-    values = torch.empty(expected, dtype=torch.float64, device=dev)
-    bad = torch.empty(1, dtype=torch.int64, device=dev)
-    _lib.check(L.wg_ascii_parse(_lib.ptr(t), n, _lib.ptr(starts), expected, _lib.ptr(values), _lib.ptr(bad),
-                                _lib.stream_ptr()), AsciiGridError)
-    first_bad = int(_device.read_small(bad)[0]) & _NO_BAD
-    if first_bad != _NO_BAD:
-        off = int(_device.read_small(starts[first_bad:first_bad + 1])[0])
+    if bad_off != _NO_BAD:
         data = full()
-        end = off
+        end = bad_off
         while end < n and data[end:end + 1] not in (b" ", b"\t", b"\n", b"\x0b", b"\x0c", b"\r", b"\x1c", b"\x1d",
-                                                   b"\x1e", b"\x1f"):
+                                                       b"\x1e", b"\x1f"):
             end += 1
-        line, col = _line_col(data, off)
-        raise AsciiGridError(f"invalid elevation value {data[off:end].decode('ascii')!r}", line=line, column=col)
-    del t, starts, scratch
+        line, col = _line_col(data, bad_off)
+        raise AsciiGridError(f"invalid elevation value {data[bad_off:end].decode('ascii')!r}", line=line, column=col)
+    del t, scratch
     try:
         return DemGrid(ncols=ncols, nrows=nrows, origin_x=header["xllcorner"], origin_y=header["yllcorner"],
                        cellsize=header["cellsize"], nodata=header["nodata_value"],

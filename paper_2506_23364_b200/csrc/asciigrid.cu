@@ -4,15 +4,16 @@
 // np.array(tokens, dtype=float64); write_ascii_grid (146-157) joins
 // format_number(v) (160-167) with single spaces, one raster row per line.
 //
-// Reader: (1) tokenise -- one pass over the body marks token starts (a
-// non-whitespace byte after whitespace; str.split()'s ASCII whitespace is
-// \t \n \v \f \r \x1c-\x1f and space), per-4-KiB-tile counts, a scan of the
-// tile counts, and a scatter of the start offsets; (2) parse -- one thread per
-// token runs nc_parse (wg_numconv.cuh: CPython float() semantics, correctly
-// rounded) and records the first invalid token.  Writer: one thread per value
-// runs nc_format (format_number: int digits or shortest round-trip repr);
-// pass 1 sums the formatted lengths per block, a scan places the blocks,
-// pass 2 formats again into shared memory and streams each block's bytes out.
+// Reader: two passes (tok_kernel, parse_kernel): token starts by SWAR
+// whitespace classification (str.split()'s ASCII whitespace is \t \n \v
+// \f \r \x1c-\x1f and space) scattered to their global index found by a
+// decoupled look-back over 4 KiB tiles, then the conversion (wg_numconv.cuh:
+// CPython float() semantics, correctly rounded) of every token, one thread
+// each, straight into its slot.
+// Writer: one fused pass (fmt_kernel): four values per thread sized and
+// formatted once (format_number: int digits or shortest round-trip repr,
+// Ryu), block byte offsets by the same look-back, bytes staged in shared
+// memory and streamed out.
 #include "wg_internal.cuh"
 
 #define NC_TABLE __device__ const
@@ -78,90 +79,6 @@ __device__ __forceinline__ unsigned start_bits(const unsigned char* __restrict__
   return ~ws & ((ws << 1) | prev) & 0xFFFFu;
 }
 
-__global__ void tok_count_kernel(const unsigned char* __restrict__ t, int64_t lo, int64_t n,
-                                 unsigned long long* __restrict__ tile_counts, unsigned* __restrict__ flags) {
-  const int64_t p0 = (int64_t)blockIdx.x * kTokTile + (int64_t)threadIdx.x * kTokBytes;
-  unsigned nonascii = 0;
-  const unsigned bits = start_bits(t, p0, lo, n, nonascii);
-  unsigned c = __popc(bits);
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  __shared__ unsigned s[kTokThreads / 32];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
-  if (__any_sync(0xffffffffu, nonascii) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long tot = 0;
-    for (int w = 0; w < kTokThreads / 32; w++) tot += s[w];
-    tile_counts[blockIdx.x] = tot;
-  }
-}
-
-// exclusive scan of n counts in place (one block of 1024); total to *total.
-// Per 1024-element chunk: warp shuffles, one shared pass over the 32 warp
-// sums, a running carry.
-__global__ void scan_kernel(unsigned long long* __restrict__ v, int64_t n, unsigned long long* __restrict__ total) {
-  __shared__ unsigned long long s_warp[32];
-  __shared__ unsigned long long s_carry;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < n; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const unsigned long long x = i < n ? v[i] : 0;
-    unsigned long long y = x;  // inclusive warp scan
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long t = __shfl_up_sync(0xffffffffu, y, o);
-      if (lane >= o) y += t;
-    }
-    if (lane == 31) s_warp[warp] = y;
-    __syncthreads();
-    if (warp == 0) {
-      const unsigned long long w = s_warp[lane];
-      unsigned long long z = w;
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, z, o);
-        if (lane >= o) z += t;
-      }
-      s_warp[lane] = z - w;  // exclusive warp offsets
-    }
-    __syncthreads();
-    const unsigned long long carry = s_carry;
-    if (i < n) v[i] = carry + s_warp[warp] + y - x;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = carry + s_warp[31] + y;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = s_carry;
-}
-
-__global__ void tok_scatter_kernel(const unsigned char* __restrict__ t, int64_t lo, int64_t n,
-                                   const unsigned long long* __restrict__ tile_offsets, int64_t* __restrict__ starts,
-                                   int64_t cap, int64_t base) {
-  const int64_t p0 = (int64_t)blockIdx.x * kTokTile + (int64_t)threadIdx.x * kTokBytes;
-  unsigned dummy = 0;
-  unsigned bits = start_bits(t, p0, lo, n, dummy);
-  const unsigned c = __popc(bits);
-  // block exclusive scan of c
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned x = c;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  __shared__ unsigned ws[kTokThreads / 32];
-  if (lane == 31) ws[warp] = x;
-  __syncthreads();
-  unsigned woff = 0;
-  for (int w = 0; w < warp; w++) woff += ws[w];
-  int64_t idx = (int64_t)tile_offsets[blockIdx.x] + woff + x - c;
-  while (bits) {
-    const int k = __ffs(bits) - 1;
-    bits &= bits - 1;
-    if (idx < cap) starts[idx] = base + p0 + k;
-    idx++;
-  }
-}
-
 // Fast path for the common numeral shape [+-]digits[.digits] (no exponent,
 // no underscore, <= 19 significant digits): the token's bytes come from six
 // word loads held in registers, the token end from a SWAR whitespace scan,
@@ -194,8 +111,135 @@ __device__ __forceinline__ bool parse_fast(const unsigned char* __restrict__ t, 
   return nc::nc_parse_simple(W, len, v, (const uint64_t(*)[2])kEL);
 }
 
+constexpr unsigned long long kFlagAgg = 1ULL << 62, kFlagIncl = 2ULL << 62, kValMask = (1ULL << 62) - 1;
+
+// lane 0: publish block bid's own total (block 0: its inclusive prefix)
+__device__ __forceinline__ void publish_aggregate(unsigned long long* status, unsigned long long bid,
+                                                  unsigned long long total) {
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    reinterpret_cast<volatile unsigned long long*>(status)[bid] = (bid == 0 ? kFlagIncl : kFlagAgg) | total;
+  }
+}
+
+// one warp: the sum of the totals of blocks 0 .. bid-1, then publishes block
+// bid's inclusive prefix.  Warp-parallel look-back: lane l inspects block
+// j - l of a 32-block window; the window is consumed up to its nearest
+// inclusive prefix once every status up to it is published.
+__device__ __forceinline__ unsigned long long resolve_prefix(unsigned long long* status, unsigned long long bid,
+                                                             unsigned long long total) {
+  const int lane = threadIdx.x & 31;
+  volatile unsigned long long* vs = status;
+  unsigned long long prefix = 0;
+  long long j = (long long)bid - 1;
+  while (j >= 0) {
+    const long long jj = j - lane;
+    const unsigned long long st = jj >= 0 ? vs[jj] : (2ULL << 62);  // before block 0: an empty inclusive prefix
+    const unsigned ready = __ballot_sync(0xffffffffu, (st & ~kValMask) != 0);
+    const unsigned incl = __ballot_sync(0xffffffffu, (st & kFlagIncl) != 0);
+    const int first_incl = incl ? __ffs(incl) - 1 : 32;  // nearest inclusive in the window
+    const unsigned need = first_incl >= 31 ? 0xffffffffu : ((2u << first_incl) - 1u);
+    if ((ready & need) != need) continue;  // a predecessor in range has not published yet
+    unsigned long long add = (lane <= first_incl && jj >= 0) ? (st & kValMask) : 0;
+    for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+    prefix += add;
+    if (first_incl < 32) break;
+    j -= 32;
+  }
+  if (lane == 0 && bid != 0) {
+    __threadfence();
+    vs[bid] = kFlagIncl | (prefix + total);
+  }
+  return prefix;
+}
+
+// Reader, pass 1 (tok_kernel): one block per 64 KiB of the body, block
+// ids in execution order (so the look-back only waits on running or finished
+// blocks): SWAR token-start bits of 16 bytes per thread, a block scan, the
+// tile's count published for the look-back, and the absolute offsets of the
+// tile's tokens scattered to starts[] at their global index.  Pass 2
+// (parse_kernel): one thread per token (parse_fast, else nc_parse), values
+// straight into out[].  info[0] = tokens in the body, info[1] = 1 if a body
+// byte is >= 0x80, info[2] = offset of token #expected (the first extra
+// token) if any, info[3] = offset of the first token < expected that float()
+// rejects (UINT64_MAX if none); pass 2 runs only when info[0] == expected.
+// kTokSub sub-tiles of 4 KiB per block: the look-back runs once per 64 KiB
+// (one look-back per 4 KiB serialises on the chain of published prefixes)
+#ifndef WG_TOK_SUB
+#define WG_TOK_SUB 16
+#endif
+constexpr int kTokSub = WG_TOK_SUB;
+
+__device__ __forceinline__ unsigned block_scan(unsigned c, unsigned* ws, unsigned& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();  // ws reuse across calls
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  unsigned woff = 0;
+  total = 0;
+  for (int w = 0; w < kTokThreads / 32; w++) {
+    if (w < warp) woff += ws[w];
+    total += ws[w];
+  }
+  return woff + x - c;  // exclusive
+}
+
+__global__ void __launch_bounds__(kTokThreads) tok_kernel(const unsigned char* __restrict__ t, int64_t lo, int64_t n,
+                                                          int64_t base, int64_t* __restrict__ starts,
+                                                          int64_t expected, unsigned long long* __restrict__ status,
+                                                          unsigned long long* __restrict__ counter,
+                                                          unsigned long long* __restrict__ info, int64_t nblocks) {
+  __shared__ unsigned ws[kTokThreads / 32];
+  __shared__ unsigned long long s_bid, s_off;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_bid = atomicAdd(counter, 1ULL);
+  __syncthreads();
+  const unsigned long long bid = s_bid;
+  const int64_t b0 = (int64_t)bid * kTokTile * kTokSub + (int64_t)threadIdx.x * kTokBytes;
+  // pass A: the block's token count
+  unsigned nonascii = 0, c = 0;
+  for (int k = 0; k < kTokSub; k++) c += __popc(start_bits(t, b0 + k * kTokTile, lo, n, nonascii));
+  if (__any_sync(0xffffffffu, nonascii) && lane == 0) atomicOr(info + 1, 1ULL);
+  unsigned total;
+  block_scan(c, ws, total);
+  if (warp == 0) {
+    publish_aggregate(status, bid, total);
+    const unsigned long long prefix = resolve_prefix(status, bid, total);
+    if (lane == 0) {
+      s_off = prefix;
+      if (bid == (unsigned long long)nblocks - 1) info[0] = prefix + total;
+    }
+  }
+  __syncthreads();
+  // pass B: sub-tile by sub-tile (document order), scatter the offsets
+  // (the bits are recomputed from the L2-resident tile: keeping all 16 in
+  // registers measured slower, 111 registers)
+  int64_t run = (int64_t)s_off;
+  for (int k = 0; k < kTokSub; k++) {
+    const int64_t p0 = b0 + k * kTokTile;
+    unsigned dummy = 0;
+    unsigned bits = start_bits(t, p0, lo, n, dummy);
+    unsigned sub;
+    int64_t idx = run + block_scan(__popc(bits), ws, sub);
+    run += sub;
+    while (bits) {
+      const int q = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (idx < expected) starts[idx] = base + p0 + q;
+      else if (idx == expected) info[2] = (unsigned long long)(base + p0 + q);
+      idx++;
+    }
+  }
+}
+
 __global__ void parse_kernel(const unsigned char* __restrict__ t, int64_t n, const int64_t* __restrict__ starts,
-                             int64_t count, double* __restrict__ out, unsigned long long* __restrict__ first_bad) {
+                             int64_t count, double* __restrict__ out, unsigned long long* __restrict__ info) {
+  if ((int64_t)info[0] != count) return;  // the host reports the count mismatch
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = starts[i];
     double v = 0.0;
@@ -205,12 +249,11 @@ __global__ void parse_kernel(const unsigned char* __restrict__ t, int64_t n, con
       while (e < n && !is_ws(__ldg(t + e))) e++;
       len = e - s;
       const int rc = len > 0x7fffffff ? -1 : nc::nc_parse(t + s, (int)len, &v, (const uint64_t(*)[2])kEL);
-      if (rc != 0) atomicMin(first_bad, (unsigned long long)i);
+      if (rc != 0) atomicMin(info + 3, (unsigned long long)s);
     }
     out[i] = v;
   }
 }
-
 
 // One pass with a decoupled look-back: block b (ids taken in execution
 // order from a counter, so every predecessor is running or done) formats its
@@ -218,7 +261,6 @@ __global__ void parse_kernel(const unsigned char* __restrict__ t, int64_t n, con
 // predecessors' counts (stopping at the first inclusive prefix) and streams
 // its bytes to their final offset.  Status word: 2 flag bits (1 = block
 // total, 2 = inclusive prefix) over a 62-bit count.
-constexpr unsigned long long kFlagAgg = 1ULL << 62, kFlagIncl = 2ULL << 62, kValMask = (1ULL << 62) - 1;
 
 __global__ void __launch_bounds__(kFmtThreads) fmt_kernel(const double* __restrict__ v, int64_t count, int64_t cols,
                                                           unsigned char* __restrict__ out,
@@ -268,35 +310,9 @@ __global__ void __launch_bounds__(kFmtThreads) fmt_kernel(const double* __restri
     total += ws[w];
   }
   if (warp == 0) {
-    // warp-parallel look-back: lane l inspects block j - l of a 32-block
-    // window; the window is consumed up to its nearest inclusive prefix once
-    // every status up to it is published
-    volatile unsigned long long* vs = status;
+    publish_aggregate(status, bid, total);
+    const unsigned long long prefix = resolve_prefix(status, bid, total);
     if (lane == 0) {
-      __threadfence();
-      vs[bid] = (bid == 0 ? kFlagIncl : kFlagAgg) | total;
-    }
-    unsigned long long prefix = 0;
-    long long j = (long long)bid - 1;
-    while (j >= 0) {
-      const long long jj = j - lane;
-      const unsigned long long st = jj >= 0 ? vs[jj] : (2ULL << 62);  // before block 0: an empty inclusive prefix
-      const unsigned ready = __ballot_sync(0xffffffffu, (st & ~kValMask) != 0);
-      const unsigned incl = __ballot_sync(0xffffffffu, (st & kFlagIncl) != 0);
-      const int first_incl = incl ? __ffs(incl) - 1 : 32;  // nearest inclusive in the window
-      const unsigned need = first_incl >= 31 ? 0xffffffffu : ((2u << first_incl) - 1u);
-      if ((ready & need) != need) continue;  // a predecessor in range has not published yet
-      unsigned long long add = (lane <= first_incl && jj >= 0) ? (st & kValMask) : 0;
-      for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-      prefix += add;
-      if (first_incl < 32) break;
-      j -= 32;
-    }
-    if (lane == 0) {
-      if (bid != 0) {
-        __threadfence();
-        vs[bid] = kFlagIncl | (prefix + total);
-      }
       s_off = prefix;
       if (bid == (unsigned long long)nblocks - 1) *nbytes = prefix + total;
     }
@@ -322,46 +338,38 @@ int64_t ntiles_of(int64_t n) { return (n + kTokTile - 1) / kTokTile; }
 
 extern "C" {
 
-size_t wg_ascii_tokenize_scratch_bytes(int64_t n) { return 256 + (size_t)(ntiles_of(n) + 1) * 8; }
-
-int wg_ascii_tokenize(const uint8_t* text, int64_t n, int64_t body_off, int64_t* starts, int64_t cap,
-                      uint64_t* count_flags, void* scratch, void* stream) {
-  if (n < 0 || body_off < 0 || body_off > n || cap < 0) return wg::set_error(WG_EARG, "bad text range");
-  if (!count_flags || !scratch || (n > 0 && !text) || (cap > 0 && !starts)) return wg::set_error(WG_EARG, "null buffer");
-  cudaStream_t st = wg::as_stream(stream);
-  // count_flags[0] = number of tokens, count_flags[1] = 1 if a byte >= 0x80
-  WG_CUDA_TRY(cudaMemsetAsync(count_flags, 0, 2 * sizeof(uint64_t), st));
-  if (n == body_off) return WG_OK;
-  const int64_t first_tile = body_off / kTokTile;
-  const int64_t tiles = ntiles_of(n) - first_tile;
-  unsigned long long* tile = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(scratch) + 256);
-  // tiles are indexed from the body's first tile: shift the text base
-  const unsigned char* t0 = text + first_tile * kTokTile;
-  const int64_t lo = body_off - first_tile * kTokTile, len = n - first_tile * kTokTile;
-  if (tiles > 0x7fffffff) return wg::set_error(WG_ELIMIT, "text too large");
-  tok_count_kernel<<<(unsigned)tiles, kTokThreads, 0, st>>>(t0, lo, len, tile,
-                                                            reinterpret_cast<unsigned*>(count_flags + 1));
-  WG_LAUNCH_CHECK("tok_count_kernel");
-  scan_kernel<<<1, 1024, 0, st>>>(tile, tiles, reinterpret_cast<unsigned long long*>(count_flags));
-  WG_LAUNCH_CHECK("scan_kernel");
-  if (cap > 0) {
-    tok_scatter_kernel<<<(unsigned)tiles, kTokThreads, 0, st>>>(t0, lo, len, tile, starts, cap,
-                                                                first_tile * kTokTile);
-    WG_LAUNCH_CHECK("tok_scatter_kernel");
-  }
-  return WG_OK;
+size_t wg_ascii_read_scratch_bytes(int64_t n, int64_t expected) {
+  return 256 + (size_t)(ntiles_of(n) + 1) * 8 + (size_t)(expected > 0 ? expected : 0) * 8;
 }
 
-int wg_ascii_parse(const uint8_t* text, int64_t n, const int64_t* starts, int64_t count, double* out,
-                   uint64_t* first_bad, void* stream) {
-  if (n < 0 || count < 0) return wg::set_error(WG_EARG, "bad text range");
-  if (!first_bad || (count > 0 && (!text || !starts || !out))) return wg::set_error(WG_EARG, "null buffer");
+int wg_ascii_read(const uint8_t* text, int64_t n, int64_t body_off, double* out, int64_t expected, uint64_t* info,
+                  void* scratch, void* stream) {
+  if (n < 0 || body_off < 0 || body_off > n || expected < 0) return wg::set_error(WG_EARG, "bad text range");
+  if (!info || !scratch || (n > 0 && !text) || (expected > 0 && !out)) return wg::set_error(WG_EARG, "null buffer");
   cudaStream_t st = wg::as_stream(stream);
-  WG_CUDA_TRY(cudaMemsetAsync(first_bad, 0xff, sizeof(uint64_t), st));
-  if (count == 0) return WG_OK;
-  parse_kernel<<<wg::stream_grid(count, 256, 8), 256, 0, st>>>(text, n, starts, count, out,
-                                                               reinterpret_cast<unsigned long long*>(first_bad));
-  WG_LAUNCH_CHECK("parse_kernel");
+  WG_CUDA_TRY(cudaMemsetAsync(info, 0, 2 * sizeof(uint64_t), st));
+  WG_CUDA_TRY(cudaMemsetAsync(info + 2, 0xff, 2 * sizeof(uint64_t), st));
+  if (n == body_off) return WG_OK;
+  // tiles are counted from the body's first tile: shift the text base
+  const int64_t first_tile = body_off / kTokTile;
+  const int64_t tiles = ntiles_of(n) - first_tile;
+  const int64_t blocks = (tiles + kTokSub - 1) / kTokSub;
+  if (blocks > 0x7fffffff) return wg::set_error(WG_ELIMIT, "text too large");
+  const unsigned char* t0 = text + first_tile * kTokTile;
+  const int64_t lo = body_off - first_tile * kTokTile, len = n - first_tile * kTokTile;
+  // scratch: [claim counter (256 B)] [tile status x tiles] [token starts x expected]
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(scratch);
+  unsigned long long* status = counter + 32;
+  int64_t* starts = reinterpret_cast<int64_t*>(status + ntiles_of(n) + 1);
+  WG_CUDA_TRY(cudaMemsetAsync(scratch, 0, 256 + (size_t)blocks * 8, st));
+  tok_kernel<<<(unsigned)blocks, kTokThreads, 0, st>>>(t0, lo, len, first_tile * kTokTile, starts, expected, status,
+                                                       counter, reinterpret_cast<unsigned long long*>(info), blocks);
+  WG_LAUNCH_CHECK("tok_kernel");
+  if (expected > 0) {
+    parse_kernel<<<wg::stream_grid(expected, 256, 8), 256, 0, st>>>(text, n, starts, expected, out,
+                                                                    reinterpret_cast<unsigned long long*>(info));
+    WG_LAUNCH_CHECK("parse_kernel");
+  }
   return WG_OK;
 }
 

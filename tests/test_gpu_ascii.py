@@ -176,3 +176,60 @@ def test_bytes_buffer_round_trip(ag):
         raw = bytes(buf)
         i = raw.rindex(b" ")
         ag.parse_ascii_grid(memoryview(raw[:i] + b" x" + raw[i + 1:]))
+
+
+def test_reader_tile_boundaries(ag):
+    """The fused reader's 4 KiB tiles: whitespace runs longer than a tile
+    (tiles without a token start), tokens longer than a tile (zero-padded
+    significands), tokens straddling tile edges at every phase, and the error
+    positions of an extra token / an invalid token far into the body."""
+    from paper_2506_23364_b200.asciigrid import _line_col
+
+    r = random.Random(9)
+    ws = [" ", "\t", "\n", "\r\n", "\x0b", "\x0c", "\x1c", "\x1f"]
+    toks, parts = [], []
+    ncols, nrows = 700, 30
+    for i in range(ncols * nrows):
+        k = r.random()
+        if k < 0.002:
+            v = r.uniform(-9, 9)
+            t = ("-" if v < 0 else "") + "0" * r.randint(4000, 9000) + repr(abs(v))  # longer than a tile
+        elif k < 0.3:
+            t = str(r.randint(-99999, 99999))
+        else:
+            t = repr(r.uniform(-5000, 5000))
+        toks.append(t)
+        sep = "".join(r.choice(ws) for _ in range(r.randint(1, 4)))
+        if r.random() < 0.003:
+            sep += " " * r.randint(4097, 12000)  # a whole tile of whitespace
+        parts.append(t + sep)
+    head = f"ncols {ncols}\nnrows {nrows}\nxllcorner 0\nyllcorner 0\ncellsize 1\nNODATA_value -9999\n"
+    doc = head + "".join(parts)
+    want = np.array([float(t) for t in toks])
+    got = np.asarray(ag.parse_ascii_grid(doc).elevations).ravel()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+    # leading whitespace so the first token starts at every phase of a tile
+    head2 = head.replace(f"ncols {ncols}\nnrows {nrows}\n", "ncols 40\nnrows 10\n")
+    for pad in (1, 7, 4095, 4096, 4097):
+        d2 = head2 + " " * pad + "".join(parts[:400])
+        g2 = np.asarray(ag.parse_ascii_grid(d2).elevations).ravel()
+        assert np.array_equal(g2.view(np.int64), want[:400].view(np.int64))
+    # one extra token: reported at its own line / column
+    j = len(parts) * 3 // 4
+    extra = head + "".join(parts[:j]) + "7 " + "".join(parts[j:])
+    off = len(extra) - len(parts[-1])  # token #expected: the last one
+    with pytest.raises(ag.AsciiGridError) as ei:
+        ag.parse_ascii_grid(extra)
+    assert (ei.value.line, ei.value.column) == _line_col(extra.encode(), off)
+    assert str(ei.value).startswith(f"expected {ncols * nrows} elevation values, found {ncols * nrows + 1}")
+    # invalid tokens far into the body: the first one is reported
+    bad = parts.copy()
+    for q in (len(bad) - 5, len(bad) // 2 + 3):
+        bad[q] = "1.2.3" + parts[q][len(toks[q]):]
+    bdoc = head + "".join(bad)
+    with pytest.raises(ag.AsciiGridError) as ei:
+        ag.parse_ascii_grid(bdoc)
+    q = len(bad) // 2 + 3
+    boff = len(head) + sum(len(p) for p in bad[:q])
+    assert str(ei.value).startswith("invalid elevation value '1.2.3'")
+    assert (ei.value.line, ei.value.column) == _line_col(bdoc.encode(), boff)

@@ -70,26 +70,22 @@ def main():
     # ---- reader: kernels only (text resident on the device)
     head_len = len(doc) - nbytes
     t = _device.upload(np.frombuffer(doc, dtype=np.uint8))
-    starts = _device.empty((count + 1,), torch.int64)
-    cf = _device.empty((2,), torch.int64)
-    sc = _device.empty((int(L.wg_ascii_tokenize_scratch_bytes(len(doc))),), torch.uint8)
+    info = _device.empty((4,), torch.int64)
+    sc = _device.empty((int(L.wg_ascii_read_scratch_bytes(len(doc), count)),), torch.uint8)
     vals = _device.empty((count,), torch.float64)
-    bad = _device.empty((1,), torch.int64)
     pt = []
     for _ in range(a.reps + 1):
         e0, e1 = events()
         e0.record()
-        L.wg_ascii_tokenize(_lib.ptr(t), len(doc), head_len, _lib.ptr(starts), count + 1, _lib.ptr(cf), _lib.ptr(sc),
-                            _lib.stream_ptr())
-        L.wg_ascii_parse(_lib.ptr(t), len(doc), _lib.ptr(starts), count, _lib.ptr(vals), _lib.ptr(bad),
-                         _lib.stream_ptr())
+        L.wg_ascii_read(_lib.ptr(t), len(doc), head_len, _lib.ptr(vals), count, _lib.ptr(info), _lib.ptr(sc),
+                        _lib.stream_ptr())
         e1.record()
         torch.cuda.synchronize()
         pt.append(e0.elapsed_time(e1))
     parse_ms = min(pt[1:])
-    assert int(_device.read_small(cf)[0]) == count
+    assert int(_device.read_small(info)[0]) == count
     assert torch.equal(vals.view(torch.int64), v.view(torch.int64)), "parse(write(g)) != g"
-    del t, starts, sc, vals
+    del t, sc, vals
 
     # ---- reader end to end: host bytes -> DemGrid (incl. H2D + validation)
     pe = []
