@@ -366,7 +366,7 @@ int wg_ascii_read(const uint8_t* text, int64_t n, int64_t body_off, double* out,
                                                        counter, reinterpret_cast<unsigned long long*>(info), blocks);
   WG_LAUNCH_CHECK("tok_kernel");
   if (expected > 0) {
-    parse_kernel<<<wg::stream_grid(expected, 256, 8), 256, 0, st>>>(text, n, starts, expected, out,
+    parse_kernel<<<wg::resident_grid(parse_kernel, expected, 256), 256, 0, st>>>(text, n, starts, expected, out,
                                                                     reinterpret_cast<unsigned long long*>(info));
     WG_LAUNCH_CHECK("parse_kernel");
   }

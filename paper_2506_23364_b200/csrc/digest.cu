@@ -126,7 +126,7 @@ extern "C" int wg_digest2d(const void* data, int64_t rows, int64_t row_bytes, in
   if (!data || ld_bytes < row_bytes) return wg::set_error(WG_EARG, "bad digest arguments");
   const int64_t W = (row_bytes + 7) / 8;
   const int64_t nthreads = rows * ((W + kTileWords - 1) / kTileWords) * 32;  // one warp per tile
-  digest_kernel<<<wg::stream_grid(nthreads, 256, 8), 256, 0, wg::as_stream(stream)>>>(
+  digest_kernel<<<wg::resident_grid(digest_kernel, nthreads, 256), 256, 0, wg::as_stream(stream)>>>(
       reinterpret_cast<const unsigned char*>(data), rows, row_bytes, ld_bytes,
       reinterpret_cast<unsigned long long*>(out));
   WG_LAUNCH_CHECK("digest_kernel");

@@ -3,6 +3,7 @@
 #include <stdio.h>
 
 #include <atomic>
+#include <mutex>
 
 #include "wg_internal.cuh"
 
@@ -34,6 +35,35 @@ int sm_count() {
       g_sms = 148;
   }
   return g_sms;
+}
+
+// Resident CTAs per SM of (kernel, block, dynamic smem), from the occupancy
+// calculator, cached per (function, block, smem).
+int resident_ctas(const void* fn, int block, size_t smem) {
+  struct Entry {
+    const void* fn;
+    int block;
+    size_t smem;
+    int ctas;
+  };
+  static Entry cache[64];
+  static std::atomic<int> used{0};
+  static std::mutex mu;
+  const int n = used.load(std::memory_order_acquire);
+  for (int i = 0; i < n; i++)
+    if (cache[i].fn == fn && cache[i].block == block && cache[i].smem == smem) return cache[i].ctas;
+  int ctas = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, block, smem) != cudaSuccess || ctas < 1) {
+    cudaGetLastError();
+    ctas = 1;
+  }
+  std::lock_guard<std::mutex> g(mu);
+  const int k = used.load(std::memory_order_relaxed);
+  if (k < 64) {
+    cache[k] = Entry{fn, block, smem, ctas};
+    used.store(k + 1, std::memory_order_release);
+  }
+  return ctas;
 }
 
 }  // namespace wg

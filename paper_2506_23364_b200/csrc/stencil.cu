@@ -373,7 +373,7 @@ extern "C" {
 int wg_grid_scan(const double* elev, int64_t n, double nodata, uint64_t* counts, void* stream) {
   if (n <= 0) return WG_OK;
   if (!elev || !counts) return wg::set_error(WG_EARG, "null buffer");
-  grid_scan_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
+  grid_scan_kernel<<<wg::resident_grid(grid_scan_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
       elev, n, nodata, reinterpret_cast<unsigned long long*>(counts));
   WG_LAUNCH_CHECK("grid_scan_kernel");
   return WG_OK;
@@ -383,7 +383,7 @@ int wg_copy2d_f64(const double* src, int64_t src_ld, double* dst, int64_t dst_ld
                   void* stream) {
   if (rows <= 0 || cols <= 0) return WG_OK;
   if (!src || !dst || src_ld < cols || dst_ld < cols) return wg::set_error(WG_EARG, "bad copy2d arguments");
-  copy2d_kernel<<<wg::stream_grid(rows * cols, kBlock), kBlock, 0, wg::as_stream(stream)>>>(src, src_ld, dst, dst_ld,
+  copy2d_kernel<<<wg::resident_grid(copy2d_kernel, rows * cols, kBlock), kBlock, 0, wg::as_stream(stream)>>>(src, src_ld, dst, dst_ld,
                                                                                              rows, cols);
   WG_LAUNCH_CHECK("copy2d_kernel");
   return WG_OK;
@@ -404,7 +404,7 @@ int wg_normals(const double* elev, int64_t nrows, int64_t ncols, double cs, doub
 int wg_steepness(const double* normals, int64_t n, double* slope, void* stream) {
   if (n <= 0) return WG_OK;
   if (!normals || !slope) return wg::set_error(WG_EARG, "null buffer");
-  steepness_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(normals, n, slope);
+  steepness_kernel<<<wg::resident_grid(steepness_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(normals, n, slope);
   WG_LAUNCH_CHECK("steepness_kernel");
   return WG_OK;
 }
@@ -412,7 +412,7 @@ int wg_steepness(const double* normals, int64_t n, double* slope, void* stream) 
 int wg_hillshade(const double* normals, int64_t n, double lx, double ly, double lz, uint8_t* out, void* stream) {
   if (n <= 0) return WG_OK;
   if (!normals || !out) return wg::set_error(WG_EARG, "null buffer");
-  hillshade_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(normals, n, lx, ly, lz, out);
+  hillshade_kernel<<<wg::resident_grid(hillshade_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(normals, n, lx, ly, lz, out);
   WG_LAUNCH_CHECK("hillshade_kernel");
   return WG_OK;
 }
@@ -421,7 +421,7 @@ int wg_hillshade_rgba(const double* normals, int64_t n, double lx, double ly, do
   if (n <= 0) return WG_OK;
   if (!normals || !out) return wg::set_error(WG_EARG, "null buffer");
   if (((uintptr_t)out) & 3) return wg::set_error(WG_EARG, "out must be 4-byte aligned");
-  hillshade_rgba_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
+  hillshade_rgba_kernel<<<wg::resident_grid(hillshade_rgba_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
       normals, n, lx, ly, lz, reinterpret_cast<uint32_t*>(out));
   WG_LAUNCH_CHECK("hillshade_rgba_kernel");
   return WG_OK;
@@ -470,7 +470,7 @@ int wg_snow(const double* elev, const double* slope, int64_t n, double base, dou
             double sl_div, int has_nodata, double nodata, uint8_t* pixels, void* stream) {
   if (n <= 0) return WG_OK;
   if (!elev || !slope || !pixels) return wg::set_error(WG_EARG, "null buffer");
-  snow_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
+  snow_kernel<<<wg::resident_grid(snow_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
       elev, slope, n, base, alt_div, top, sl_div, has_nodata, nodata, reinterpret_cast<uchar4*>(pixels));
   WG_LAUNCH_CHECK("snow_kernel");
   return WG_OK;
@@ -479,7 +479,7 @@ int wg_snow(const double* elev, const double* slope, int64_t n, double base, dou
 int wg_runout_stats(const int64_t* hits, const double* zmax, int64_t n, uint64_t* out, void* stream) {
   if (n <= 0) return WG_OK;
   if (!hits || !zmax || !out) return wg::set_error(WG_EARG, "null buffer");
-  runout_stats_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
+  runout_stats_kernel<<<wg::resident_grid(runout_stats_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(
       reinterpret_cast<const long long*>(hits), zmax, n, reinterpret_cast<unsigned long long*>(out));
   WG_LAUNCH_CHECK("runout_stats_kernel");
   return WG_OK;
@@ -488,7 +488,7 @@ int wg_runout_stats(const int64_t* hits, const double* zmax, int64_t n, uint64_t
 int wg_synth_combine(const double* rowf, const double* colf, const double* lin, int noct, int64_t nrows,
                      int64_t ncols, double* elev, void* stream) {
   if (nrows * ncols <= 0) return WG_OK;
-  synth_kernel<<<wg::stream_grid(nrows * ncols, kBlock), kBlock, 0, wg::as_stream(stream)>>>(rowf, colf, lin, noct,
+  synth_kernel<<<wg::resident_grid(synth_kernel, nrows * ncols, kBlock), kBlock, 0, wg::as_stream(stream)>>>(rowf, colf, lin, noct,
                                                                                               nrows, ncols, elev);
   WG_LAUNCH_CHECK("synth_kernel");
   return WG_OK;
@@ -496,7 +496,7 @@ int wg_synth_combine(const double* rowf, const double* colf, const double* lin, 
 
 int wg_sub_scalar(double* elev, int64_t n, double v, void* stream) {
   if (n <= 0) return WG_OK;
-  sub_scalar_kernel<<<wg::stream_grid(n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(elev, n, v);
+  sub_scalar_kernel<<<wg::resident_grid(sub_scalar_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(elev, n, v);
   WG_LAUNCH_CHECK("sub_scalar_kernel");
   return WG_OK;
 }

@@ -16,11 +16,15 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count();
 
-// Grid size for a streaming (HBM-bound) kernel: enough resident CTAs to cover
-// every SM several times, never more blocks than work.
-inline int stream_grid(int64_t work_items, int block, int ctas_per_sm = 8) {
+// Grid for a grid-stride kernel: exactly the CTAs that are resident at once
+// (occupancy calculator: registers, shared memory, block size), never more
+// than the work needs -- one balanced wave, no tail wave of leftover blocks.
+int resident_ctas(const void* fn, int block, size_t smem);
+
+template <typename Kernel>
+inline int resident_grid(Kernel* kernel, int64_t work_items, int block, size_t smem = 0) {
   int64_t want = (work_items + block - 1) / block;
-  int64_t cap = (int64_t)sm_count() * ctas_per_sm;
+  const int64_t cap = (int64_t)sm_count() * resident_ctas(reinterpret_cast<const void*>(kernel), block, smem);
   if (want > cap) want = cap;
   if (want < 1) want = 1;
   return (int)want;

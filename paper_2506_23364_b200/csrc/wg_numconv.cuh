@@ -443,8 +443,12 @@ NC_HD uint64_t bytes8(const uint64_t* W, int off) {
     const uint64_t fill = k >= 8 ? ~0ULL : ((1ULL << (8 * k)) - 1);
     return x | (0x3030303030303030ULL & fill);
   }
+  // word selection by compare/select on constant indices (W stays in
+  // registers; a dynamic W[q] would place the array in local memory)
   const int q = off >> 3, r = off & 7;
-  return r == 0 ? W[q] : (W[q] >> (8 * r)) | (W[q + 1] << (64 - 8 * r));
+  const uint64_t lo = q == 0 ? W[0] : (q == 1 ? W[1] : W[2]);
+  const uint64_t hi = q == 0 ? W[1] : (q == 1 ? W[2] : W[3]);
+  return (lo >> (8 * r)) | ((hi << 1) << (63 - 8 * r));  // r == 0: hi << 64 -> 0
 }
 
 NC_HD bool eight_digits(uint64_t x) {
@@ -501,8 +505,11 @@ NC_HD bool nc_parse_simple(const uint64_t* W, int len, double* out, const uint64
   if (ni < 0 || ni + nf < 1 || ni > 16 || nf > 16 || ni + nf > 19) return false;
   uint64_t iv, fv;
   if (!digits_value(W, s0, ni, iv) || !digits_value(W, p + 1, nf, fv)) return false;
-  uint64_t scale = 1;
-  for (int k = 0; k < nf; k++) scale *= 10;
+  uint64_t scale = (nf & 1) ? 10 : 1;  // 10^nf, nf <= 16
+  if (nf & 2) scale *= 100;
+  if (nf & 4) scale *= 10000;
+  if (nf & 8) scale *= 100000000;
+  if (nf & 16) scale *= 10000000000000000ULL;
   const uint64_t m = iv * scale + fv;
   const uint64_t bits = m == 0 ? 0 : el_convert(-(int64_t)nf, m, tab);
   *out = bits_to_double(bits | (c0 == '-' ? 0x8000000000000000ULL : 0));
