@@ -41,10 +41,10 @@ BYTES_PER_STEP = 64  # 32 B DEM patch + 16 B hit RMW + 16 B drop
 # FP64-pipe instructions per particle-step (DFMA+DMUL+DADD+DSETP per active
 # thread) from the ncu SASS capture of traj_kernel (profiles/r01_traj_ncu_summary.txt),
 # and the measured FP64 instruction peak (profiles/fp64_peak.json, DADD/DMUL rate)
-FP64_OPS_PER_STEP = 180  # 154 DFMA+DMUL+DADD + 26 DSETP (ncu source page, r01 final build)
+FP64_OPS_PER_STEP = 170  # 146 DFMA+DMUL+DADD + 24 DSETP (ncu source page, r01 final build)
 FP64_PEAK_OPS = 1.853e13
 # DRAM bytes per traj_kernel launch from ncu --set full (dram__bytes_read+write, r01)
-TRAJ_DRAM_BYTES = 6.65e9
+TRAJ_DRAM_BYTES = 6.61e9
 
 
 def parse():
