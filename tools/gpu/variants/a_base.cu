@@ -179,20 +179,27 @@ __device__ __forceinline__ void sincos_glibc(const double* tab, double x, double
   const double u = WG_ADD(WG_SC_BIG, ax);
   const int k = (int)((uint32_t)wg_bits(u) << 2);
   const double xr = WG_SUB(ax, WG_SUB(u, WG_SC_BIG));
-  const double dsn = (x <= 0.0) ? -0.0 : 0.0;  // do_sin: if (x <= 0) dx = -dx
-  const double dcs = (x < 0.0) ? -0.0 : 0.0;   // do_cos: if (x < 0) dx = -dx
-  const double xc = WG_ADD(xr, dcs);            // do_cos's reduced argument
   const double2 t01 = *reinterpret_cast<const double2*>(tab + k);      // sn, ssn
   const double2 t23 = *reinterpret_cast<const double2*>(tab + k + 2);  // cs, ccs
   const double sn = t01.x, ssn = t01.y, cs = t23.x, ccs = t23.y;
+  // glibc adds a signed zero to the reduced argument (do_sin: -0 if x <= 0,
+  // do_cos: -0 if x < 0) and folds one into the sine's correction term.
+  // Those only change the SIGN OF A ZERO intermediate (xr == 0 exactly), and
+  // a zero's sign cannot reach either result: the table sine is used only
+  // for |x| >= 0.126, where sn != 0 absorbs a signed-zero correction
+  // (sn + -0 == sn + +0), and the cosine always adds to cs >= cos(0.86) > 0.
+  // Hence both paths run on xr itself and share xx, x*xx and the
+  // polynomial terms (bit-identical results; tests/test_gpu_parity.py covers
+  // grid points k/128, where xr == 0).
+  const double xx = WG_MUL(xr, xr);
+  const double xxx = WG_MUL(xr, xx);
+  const double ps = WG_FMA(xx, WG_SC_SN5, WG_SC_SN3);
+  double pc = WG_FMA(xx, WG_SC_CS6, WG_SC_CS4);
+  pc = WG_FMA(xx, pc, WG_SC_CS2);
+  const double cc = WG_MUL(xx, pc);
   double st;
   {  // do_sin(x, 0), table path
-    const double xx = WG_MUL(xr, xr);
-    const double ps = WG_FMA(xx, WG_SC_SN5, WG_SC_SN3);
-    const double ss = WG_ADD(xr, WG_FMA(WG_MUL(xr, xx), ps, dsn));
-    double pc = WG_FMA(xx, WG_SC_CS6, WG_SC_CS4);
-    pc = WG_FMA(xx, pc, WG_SC_CS2);
-    const double cc = WG_FMA(xr, dsn, WG_MUL(xx, pc));
+    const double ss = WG_ADD(xr, WG_MUL(xxx, ps));
     double cor = WG_FMA(ss, ccs, ssn);
     cor = WG_FMA(wg_neg(cc), sn, cor);
     cor = WG_FMA(ss, cs, cor);
@@ -200,22 +207,17 @@ __device__ __forceinline__ void sincos_glibc(const double* tab, double x, double
   }
   double sy;
   {  // do_sin(x, 0), Taylor branch (TAYLOR_SIN(x*x, x, 0))
-    const double xx = WG_MUL(x, x);
-    double p = WG_FMA(xx, WG_SC_S5, WG_SC_S4);
-    p = WG_FMA(xx, p, WG_SC_S3);
-    p = WG_FMA(xx, p, WG_SC_S2);
-    p = WG_FMA(xx, p, WG_SC_S1);
+    const double xt = WG_MUL(x, x);
+    double p = WG_FMA(xt, WG_SC_S5, WG_SC_S4);
+    p = WG_FMA(xt, p, WG_SC_S3);
+    p = WG_FMA(xt, p, WG_SC_S2);
+    p = WG_FMA(xt, p, WG_SC_S1);
     double t = WG_FMA(p, x, -0.0);
-    t = WG_FMA(xx, t, 0.0);
+    t = WG_FMA(xt, t, 0.0);
     sy = WG_ADD(x, t);
   }
   {  // do_cos(x, 0)
-    const double xx = WG_MUL(xc, xc);
-    const double ps = WG_FMA(xx, WG_SC_SN5, WG_SC_SN3);
-    const double ss = WG_FMA(WG_MUL(xc, xx), ps, xc);
-    double pc = WG_FMA(xx, WG_SC_CS6, WG_SC_CS4);
-    pc = WG_FMA(xx, pc, WG_SC_CS2);
-    const double cc = WG_MUL(xx, pc);
+    const double ss = WG_FMA(xxx, ps, xr);
     double cor = WG_FMA(wg_neg(ss), ssn, ccs);
     cor = WG_FMA(wg_neg(cc), cs, cor);
     cor = WG_FMA(wg_neg(ss), sn, cor);
@@ -793,9 +795,9 @@ int launch_traj(World w, Work& wk, void* scratch, cudaStream_t st) {
   WG_CUDA_TRY(cudaMemsetAsync(wk.cursor, 0, 2 * sizeof(unsigned long long), st));
   w.absmax_bits = wk.cursor + 1;
   const int64_t ncells = (int64_t)w.nrows * w.ncols;
-  absmax_kernel<<<wg::stream_grid(ncells, 256, 4), 256, 0, st>>>(w.e, ncells, wk.cursor + 1);
+  absmax_kernel<<<wg::resident_grid(absmax_kernel, ncells, 256), 256, 0, st>>>(w.e, ncells, wk.cursor + 1);
   WG_LAUNCH_CHECK("absmax_kernel");
-  prep_kernel<kAccum><<<wg::stream_grid(nk, 128, 4), 128, 0, st>>>(w, wk, nk, starts);
+  prep_kernel<kAccum><<<wg::resident_grid(prep_kernel<kAccum>, nk, 128), 128, 0, st>>>(w, wk, nk, starts);
   WG_LAUNCH_CHECK("prep_kernel");
   auto kern = traj_kernel<kAccum, kRecords>;
   int per_sm = 0;
@@ -903,7 +905,7 @@ int wg_trace_particle(const double* dem, int64_t nrows, int64_t ncols, double ox
 int wg_trig_eval(const double* x, int64_t n, double* s, double* c, void* stream) {
   if (n <= 0) return WG_OK;
   if (!x || !s || !c) return wg::set_error(WG_EARG, "null buffer");
-  trig_eval_kernel<<<wg::stream_grid(n, 256), 256, 0, wg::as_stream(stream)>>>(x, n, s, c);
+  trig_eval_kernel<<<wg::resident_grid(trig_eval_kernel, n, 256), 256, 0, wg::as_stream(stream)>>>(x, n, s, c);
   WG_LAUNCH_CHECK("trig_eval_kernel");
   return WG_OK;
 }
@@ -911,7 +913,7 @@ int wg_trig_eval(const double* x, int64_t n, double* s, double* c, void* stream)
 int wg_sqrt_eval(const double* x, int64_t n, double* r, int8_t* fast, void* stream) {
   if (n <= 0) return WG_OK;
   if (!x || !r || !fast) return wg::set_error(WG_EARG, "null buffer");
-  sqrt_eval_kernel<<<wg::stream_grid(n, 256), 256, 0, wg::as_stream(stream)>>>(x, n, r, fast);
+  sqrt_eval_kernel<<<wg::resident_grid(sqrt_eval_kernel, n, 256), 256, 0, wg::as_stream(stream)>>>(x, n, r, fast);
   WG_LAUNCH_CHECK("sqrt_eval_kernel");
   return WG_OK;
 }
@@ -919,7 +921,7 @@ int wg_sqrt_eval(const double* x, int64_t n, double* r, int8_t* fast, void* stre
 int wg_div_eval(const double* a, const double* b, int64_t n, double* q, void* stream) {
   if (n <= 0) return WG_OK;
   if (!a || !b || !q) return wg::set_error(WG_EARG, "null buffer");
-  div_eval_kernel<<<wg::stream_grid(n, 256), 256, 0, wg::as_stream(stream)>>>(a, b, n, q);
+  div_eval_kernel<<<wg::resident_grid(div_eval_kernel, n, 256), 256, 0, wg::as_stream(stream)>>>(a, b, n, q);
   WG_LAUNCH_CHECK("div_eval_kernel");
   return WG_OK;
 }
