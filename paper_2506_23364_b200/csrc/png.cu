@@ -13,14 +13,16 @@
 //                  Up/Avg/Paeth) with the least sum of |signed residual|
 //                  (libpng's heuristic); writes the filtered stream (filter
 //                  byte + residuals per row) and its Adler-32;
-//   lz_kernel      one warp per ~32 KiB chunk of rows: greedy LZ77 parse
-//                  with a 32-position lookahead (lane k measures position
-//                  i + k; the first match ends the step).
+//   lz_kernel      one warp per ~32 KiB chunk of rows: LZ77 parse with a
+//                  32-position lookahead (lane k checks position i + k; the
+//                  first match ends the step) and one-step lazy evaluation
+//                  (half the warp measures the match one byte later).
 //                  Candidates per position: the 4 most recent positions with
 //                  the same 3-byte hash (a per-chunk bucket table in global
-//                  memory, inserted warp-parallel, one writer per bucket and
-//                  token so the parse is deterministic) and the image-shaped
-//                  distances 1, 4, row, 2 rows, row +- 4; each lane measures
+//                  memory, every consumed position inserted warp-parallel,
+//                  one writer per bucket so the parse is deterministic) and
+//                  the image-shaped distances 1, 4, row, 2 rows, row +- 4;
+//                  each lane measures
 //                  one candidate, the warp keeps the longest (ties: the
 //                  lowest lane); matches may reach back 32 KiB into earlier
 //                  chunks.  Tokens go to a per-chunk array;
@@ -225,13 +227,27 @@ struct Layout {
   int64_t f_off, tok_off, tab_off, meta_off, per_image;
 };
 
-constexpr int kBuckets = 1024;  // per chunk, 4 slots each
+// LZ77 knobs (A/B on the 1365-tile bench, hillshade / overlay ms and mean
+// KB: base (10 hash bits, first-32 inserts, greedy) 71.7 / 114.3 ms, 40.7 /
+// 82.7 KB; + 12 hash bits, every consumed position inserted, one-step lazy
+// evaluation: 68.6 / 118.3 ms, 40.5 / 80.5 KB; + 8 slots: 74.5 / 149.3 ms,
+// 38.5 / 80.0 KB)
+#ifndef WG_PNG_HBITS
+#define WG_PNG_HBITS 12
+#endif
+#ifndef WG_PNG_INSERT_ALL
+#define WG_PNG_INSERT_ALL 1
+#endif
+#ifndef WG_PNG_LAZY
+#define WG_PNG_LAZY 1
+#endif
+constexpr int kHashBits = WG_PNG_HBITS;
+constexpr int kBuckets = 1 << kHashBits;  // per chunk
 #ifndef WG_PNG_SLOTS
 #define WG_PNG_SLOTS 4
 #endif
-// most recent positions per bucket: 4 or 8 (A/B: 8 gives 5 % smaller
-// hillshade tiles but runs the runout overlay 26 % slower; lazy matching
-// measured no gain)
+// most recent positions per bucket: 4 or 8 (8: 5 % smaller hillshade tiles,
+// the runout overlay 26 % slower)
 constexpr int kSlots = WG_PNG_SLOTS;
 constexpr int kSlotVecs = kSlots / 4;  // uint4 per bucket
 constexpr int kWindow = 32768;
@@ -326,7 +342,7 @@ __global__ void __launch_bounds__(kPngThreads) filter_kernel(Batch b) {
 // ---- kernel 2: LZ77 parse, one warp per chunk ------------------------------
 __device__ __forceinline__ uint32_t hash3(const uint8_t* F, int64_t p) {
   const uint32_t v = (uint32_t)F[p] | ((uint32_t)F[p + 1] << 8) | ((uint32_t)F[p + 2] << 16);
-  return (v * 2654435761u) >> (32 - 10);  // kBuckets = 2^10
+  return (v * 2654435761u) >> (32 - kHashBits);
 }
 
 // 4 bytes of F starting at byte x (little endian; F is 4-byte aligned and
@@ -351,6 +367,9 @@ __device__ __forceinline__ int match_len(const uint8_t* F, int64_t q, int64_t p,
 }
 
 constexpr int kCands = kSlots + 6;
+constexpr bool kLazy = WG_PNG_LAZY != 0;
+constexpr bool kInsertAll = WG_PNG_INSERT_ALL != 0;
+static_assert(!kLazy || kCands <= 16, "lazy evaluation uses 16 lanes per position");
 
 // candidate k (0..kCands) for position p: the bucket's slots (as of the
 // current step), then the image-shaped distances 1, 4, row, 2 rows, row +- 4
@@ -375,13 +394,15 @@ __device__ __forceinline__ int64_t candidate(const uint8_t* F, int64_t p, int k,
 
 __device__ __forceinline__ bool valid_cand(int64_t q, int64_t p) { return q >= 0 && q < p && p - q <= kWindow; }
 
-// Greedy LZ77 over one chunk with a 32-position lookahead.  Phase 1: lane k
+// LZ77 over one chunk with a 32-position lookahead.  Phase 1: lane k
 // checks whether any candidate of position i + k shares its first 3 bytes;
 // the first such lane f ends the step (the lanes before it are literals),
 // so incompressible stretches advance 32 bytes per step.  Phase 2: lanes
 // 0..kCands-1 each extend one candidate of position i + f (4-byte
-// compares); the longest wins (ties: the earlier candidate).  Positions are
-// inserted after each step, one writer per bucket (deterministic).
+// compares), lanes 16.. those of i + f + 1 (lazy); the longest wins (ties:
+// the earlier candidate), and a strictly longer match at i + f + 1 makes
+// i + f a literal.  Positions are inserted after each step, one writer per
+// bucket (deterministic).
 __global__ void __launch_bounds__(256) lz_kernel(Batch b, int64_t nwork) {
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wid >= nwork) return;
@@ -417,39 +438,61 @@ __global__ void __launch_bounds__(256) lz_kernel(Batch b, int64_t nwork) {
     int64_t adv = f;
     if (hit) {
       const int64_t pf = i + f;
-      const int maxl = (int)(end - pf < 258 ? end - pf : 258);
+      // lanes 0-15 extend the candidates of pf; with WG_PNG_LAZY lanes 16-31
+      // those of pf + 1 (one-step lazy evaluation: a longer match one byte
+      // later turns pf into a literal, as zlib's deflate_slow)
+      const int half = kLazy ? (lane >> 4) : 0;
+      const int k = kLazy ? (lane & 15) : lane;
+      const int64_t pp = pf + half;
+      const int maxl = (int)(end - pp < 258 ? end - pp : 258);
       int len = 0;
       int64_t q = -1;
-      if (lane < kCands) {
-        q = candidate(F, pf, lane, S, tab, nbytes);
-        if (valid_cand(q, pf)) len = match_len(F, q, pf, maxl);
+      if (k < kCands && maxl >= 3) {
+        q = candidate(F, pp, k, S, tab, nbytes);
+        if (valid_cand(q, pp)) len = match_len(F, q, pp, maxl);
       }
-      const unsigned key = ((unsigned)len << 8) | (unsigned)(31 - lane);
-      unsigned best = key;
-      for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-      const int mlen = (int)(best >> 8);
-      const int64_t mq = __shfl_sync(0xffffffffu, q, 31 - (int)(best & 255u));
-      if (lane == 0) out[ntok + f] = ((uint32_t)mlen << 16) | (uint32_t)(pf - mq - 1);
-      ntok += f + 1;
-      adv += mlen;
+      unsigned best = ((unsigned)len << 8) | (unsigned)(31 - lane);
+      for (int o = kLazy ? 8 : 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      const unsigned best0 = __shfl_sync(0xffffffffu, best, 0);
+      const unsigned best1 = kLazy ? __shfl_sync(0xffffffffu, best, 16) : 0u;
+      const bool later = kLazy && (best1 >> 8) > (best0 >> 8) && (best1 >> 8) >= 3;
+      const unsigned bw = later ? best1 : best0;
+      const int mlen = (int)(bw >> 8);
+      const int64_t mq = __shfl_sync(0xffffffffu, q, 31 - (int)(bw & 255u));
+      if (later) {
+        if (lane == 0) {
+          out[ntok + f] = F[pf];
+          out[ntok + f + 1] = ((uint32_t)mlen << 16) | (uint32_t)(pf + 1 - mq - 1);
+        }
+        ntok += f + 2;
+        adv += 1 + mlen;
+      } else {
+        if (lane == 0) out[ntok + f] = ((uint32_t)mlen << 16) | (uint32_t)(pf - mq - 1);
+        ntok += f + 1;
+        adv += mlen;
+      }
     } else {
       ntok += f;
     }
-    // insert the consumed positions (the first 32), newest per bucket wins
-    const int nins = adv < 32 ? (int)adv : 32;
-    const bool ins = lane < nins && p + 2 < nbytes;
-    const uint32_t h = ins ? hash3(F, p) : 0xFFFFFFFFu - lane;
-    const unsigned grp = __match_any_sync(0xffffffffu, h);
-    if (ins && (31 - __clz(grp)) == lane) {
-      uint4* bk = tab + (int64_t)h * kSlotVecs;
-      const uint4 e = bk[0];
-      if (kSlotVecs == 2) {
-        const uint4 f = bk[1];
-        bk[1] = make_uint4(e.w, f.x, f.y, f.z);
+    // insert the consumed positions (the first 32, or all with
+    // WG_PNG_INSERT_ALL), newest per bucket wins
+    for (int64_t b0 = 0; b0 < (kInsertAll ? adv : 1); b0 += 32) {
+      const int64_t pi = i + b0 + lane;
+      const int nins = adv - b0 < 32 ? (int)(adv - b0) : 32;
+      const bool ins = lane < nins && pi + 2 < nbytes;
+      const uint32_t h = ins ? hash3(F, pi) : 0xFFFFFFFFu - lane;
+      const unsigned grp = __match_any_sync(0xffffffffu, h);
+      if (ins && (31 - __clz(grp)) == lane) {
+        uint4* bk = tab + (int64_t)h * kSlotVecs;
+        const uint4 e = bk[0];
+        if (kSlotVecs == 2) {
+          const uint4 f = bk[1];
+          bk[1] = make_uint4(e.w, f.x, f.y, f.z);
+        }
+        bk[0] = make_uint4((uint32_t)(pi + 1), e.x, e.y, e.z);
       }
-      bk[0] = make_uint4((uint32_t)(p + 1), e.x, e.y, e.z);
+      __syncwarp();
     }
-    __syncwarp();
     i += adv;
   }
   if (lane == 0) counts[ch] = (uint32_t)ntok;
