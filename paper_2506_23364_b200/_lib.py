@@ -49,10 +49,11 @@ SIGNATURES: dict[str, tuple] = {
     "wg_avalanche_scratch_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "wg_run_avalanche": (
         c_int,
-        [c_ptr, c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_i64,
-         c_ptr, c_i64, c_u64, c_i64, c_i64, c_i64, c_int, c_int, c_ptr, c_ptr, c_ptr, c_ptr],
+        [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl,
+         c_i64, c_ptr, c_i64, c_u64, c_i64, c_i64, c_i64, c_int, c_int, c_ptr, c_ptr, c_ptr, c_ptr],
     ),
     "wg_build_quad": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
+    "wg_build_pair": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
     "wg_trace_particle": (
         c_int,
         [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_i64,

@@ -336,20 +336,46 @@ def _world() -> tuple[int, int]:
     return 0, 1
 
 
+_LAYOUT_HEADROOM = 4 << 30  # free HBM kept for scratch after a gather layout
+
+
 def build_quad(grid: DemGrid) -> torch.Tensor | None:
     """Patch-corner layout of the DEM (wg_build_quad: 32 B per cell, four
     times the DEM) so every particle step gathers its bilinear patch with one
-    256-bit load; None when it would not fit comfortably (the kernel then
-    gathers from the plain DEM, same results)."""
+    256-bit load; None when it would not fit (see build_gather_layout)."""
     need = grid.nrows * grid.ncols * 32
     free, _ = torch.cuda.mem_get_info()
-    if need > free // 2:
+    if need > free - _LAYOUT_HEADROOM:
         return None
     L = _lib.lib()
     quad = _device.empty((grid.nrows * grid.ncols * 4,), torch.float64)
     _lib.check(L.wg_build_quad(_lib.ptr(grid.device_elevations()), grid.nrows, grid.ncols, _lib.ptr(quad),
                                _lib.stream_ptr()), ParamError)
     return quad
+
+
+def build_pair(grid: DemGrid) -> torch.Tensor | None:
+    """Row-pair layout of the DEM (wg_build_pair: 16 B per cell, twice the
+    DEM): two 128-bit loads per step; None when it would not fit."""
+    need = grid.nrows * grid.ncols * 16
+    free, _ = torch.cuda.mem_get_info()
+    if need > free - _LAYOUT_HEADROOM:
+        return None
+    L = _lib.lib()
+    pair = _device.empty((grid.nrows * grid.ncols * 2,), torch.float64)
+    _lib.check(L.wg_build_pair(_lib.ptr(grid.device_elevations()), grid.nrows, grid.ncols, _lib.ptr(pair),
+                               _lib.stream_ptr()), ParamError)
+    return pair
+
+
+def build_gather_layout(grid: DemGrid) -> tuple[torch.Tensor | None, torch.Tensor | None]:
+    """(quad, pair) for the trajectory gather: the patch-corner quads when
+    they fit, else the row pairs, else neither (four loads from the DEM).
+    The results are identical for every layout."""
+    quad = build_quad(grid)
+    if quad is not None:
+        return quad, None
+    return None, build_pair(grid)
 
 
 def run_avalanche_device(
@@ -380,10 +406,10 @@ def run_avalanche_device(
     scratch = _device.empty((int(L.wg_avalanche_scratch_bytes(params.particles_per_release_cell, int(i_lo),
                                                                int(i_hi))),), torch.uint8)
     dem = grid.device_elevations()
-    quad = build_quad(grid) if int(i_hi) > int(i_lo) else None
+    quad, pair = build_gather_layout(grid) if int(i_hi) > int(i_lo) else (None, None)
     _lib.check(
         L.wg_run_avalanche(
-            _lib.ptr(dem), _lib.ptr(quad), *_sc_args(sc), _lib.ptr(cells), params.particles_per_release_cell,
+            _lib.ptr(dem), _lib.ptr(quad), _lib.ptr(pair), *_sc_args(sc), _lib.ptr(cells), params.particles_per_release_cell,
             rng.seed_word(params.seed), int(i_lo), int(i_hi), int(shard_block), int(rank), int(nranks),
             _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(scratch), _lib.stream_ptr(stream),
         ),

@@ -13,6 +13,7 @@ import torch  # noqa: E402
 
 import paper_2506_23364_b200 as wf  # noqa: E402
 from paper_2506_23364_b200 import _lib  # noqa: E402
+from paper_2506_23364_b200 import simulate  # noqa: E402
 from paper_2506_23364_b200.simulate import build_quad, release_cells, run_avalanche_device  # noqa: E402
 from paper_2506_23364_b200.synth import synth_dem_device  # noqa: E402
 from paper_2506_23364_b200.terrain import compute_normals_and_slope  # noqa: E402
@@ -75,6 +76,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--records", action="store_true", help="also report particle lifetime stats")
+    ap.add_argument("--layout", choices=["auto", "pair", "dem"], default="auto", help="force the gather layout")
     a = ap.parse_args()
     _lib.build()
     elev = synth_dem_device(a.size, a.seed)
@@ -85,7 +87,10 @@ def main():
     cells = release_cells(mask)
     hits = torch.zeros((a.size, a.size), dtype=torch.int64, device="cuda")
     zmax = torch.zeros((a.size, a.size), dtype=torch.float64, device="cuda")
-    quad_ok = build_quad(grid) is not None
+    quad_ok = build_quad(grid) is not None and a.layout == "auto"
+    if a.layout != "auto":
+        simulate.build_gather_layout = (lambda g: (None, simulate.build_pair(g))) if a.layout == "pair" \
+            else (lambda g: (None, None))
     times = []
     clocks = []
     try:
@@ -110,7 +115,7 @@ def main():
         times.append(round(e0.elapsed_time(e1), 2))
     steps = int(hits.sum().item()) - int(cells.numel()) * a.ppc
     out = {"cells": int(cells.numel()), "particles": int(cells.numel()) * a.ppc, "steps": steps,
-           "quad": quad_ok, "ms": times, "clocks": clocks, "gsteps_s_best": round(steps / min(times) / 1e6, 2)}
+           "quad": quad_ok, "layout": a.layout, "ms": times, "clocks": clocks, "gsteps_s_best": round(steps / min(times) / 1e6, 2)}
     if a.records:
         from paper_2506_23364_b200.simulate import particle_records
 
