@@ -66,6 +66,7 @@ constexpr int kMinBlocksPerSM = WG_TRAJ_MINBLOCKS;  // 8: 64 registers, no spill
 struct World {
   const double* __restrict__ e;
   const double* __restrict__ quad;  // nullable: per-patch corner quads (wg_build_quad)
+  const double* __restrict__ pair;  // nullable: per-cell (south, north) pairs (wg_build_pair)
   int nrows, ncols;
   double ox, oy, cs, xmax, ymax;
   double cmax, rmax;  // ncols - 1.0, nrows - 1.0 (exact)
@@ -295,6 +296,10 @@ __device__ __forceinline__ void sample(const World& w, double rcs, double x, dou
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(z00), "=d"(z10), "=d"(z01), "=d"(z11)
         : "l"(w.quad + 4 * patch));
+  } else if (w.pair != nullptr) {
+    // (z00, z01) and (z10, z11): two adjacent 128-bit loads (wg_build_pair)
+    asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(z00), "=d"(z01) : "l"(w.pair + 2 * patch));
+    asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(z10), "=d"(z11) : "l"(w.pair + 2 * patch + 2));
   } else {
     const double* south = w.e + patch;
     const double* north = south - w.ncols;
@@ -679,6 +684,20 @@ __global__ void quad_kernel(const double* __restrict__ e, int nrows, int ncols, 
   }
 }
 
+// Row-pair layout (half the footprint of the quads, for grids where those do
+// not fit): pair[i * ncols + j] = (e[i][j], e[i-1][j]) for i >= 1; a patch is
+// the two adjacent pairs at (i, j) and (i, j + 1).
+__global__ void pair_kernel(const double* __restrict__ e, int nrows, int ncols, double2* __restrict__ pair) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  for (int i = 1 + blockIdx.y; i < nrows; i += gridDim.y) {
+    const double* s = e + (int64_t)i * ncols + j;
+    const double a = __ldg(s), b = __ldg(s - ncols);
+    asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(pair + (int64_t)i * ncols + j), "d"(a), "d"(b)
+                 : "memory");
+  }
+}
+
 __global__ void div_eval_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
                                 double* __restrict__ q) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -712,6 +731,7 @@ World make_world(const double* dem, int64_t nrows, int64_t ncols, double ox, dou
   World w;
   w.e = dem;
   w.quad = nullptr;
+  w.pair = nullptr;
   w.nrows = (int)nrows;
   w.ncols = (int)ncols;
   w.ox = ox;
@@ -826,16 +846,24 @@ int wg_build_quad(const double* dem, int64_t nrows, int64_t ncols, double* quad,
   int rc = check_world(dem, nrows, ncols, 1.0);
   if (rc) return rc;
   if (quad == nullptr || (((uintptr_t)quad) & 31) != 0) return wg::set_error(WG_EARG, "quad must be 32-byte aligned");
-  const int64_t n = nrows * ncols;
-  (void)n;
   const dim3 grid((unsigned)((ncols + 255) / 256), (unsigned)(nrows < 4096 ? nrows : 4096));
   quad_kernel<<<grid, 256, 0, wg::as_stream(stream)>>>(dem, (int)nrows, (int)ncols, reinterpret_cast<double4*>(quad));
   WG_LAUNCH_CHECK("quad_kernel");
   return WG_OK;
 }
 
-int wg_run_avalanche(const double* dem, const double* dem_quad, int64_t nrows, int64_t ncols, double ox, double oy,
-                     double cs, double xmax, double ymax, double tana, double p, double omp, double rscale, double rh,
+int wg_build_pair(const double* dem, int64_t nrows, int64_t ncols, double* pair, void* stream) {
+  int rc = check_world(dem, nrows, ncols, 1.0);
+  if (rc) return rc;
+  if (pair == nullptr || (((uintptr_t)pair) & 15) != 0) return wg::set_error(WG_EARG, "pair must be 16-byte aligned");
+  const dim3 grid((unsigned)((ncols + 255) / 256), (unsigned)(nrows < 4096 ? nrows : 4096));
+  pair_kernel<<<grid, 256, 0, wg::as_stream(stream)>>>(dem, (int)nrows, (int)ncols, reinterpret_cast<double2*>(pair));
+  WG_LAUNCH_CHECK("pair_kernel");
+  return WG_OK;
+}
+
+int wg_run_avalanche(const double* dem, const double* dem_quad, const double* dem_pair, int64_t nrows, int64_t ncols,
+                     double ox, double oy, double cs, double xmax, double ymax, double tana, double p, double omp, double rscale, double rh,
                      int64_t max_steps, const int64_t* cells, int64_t per_cell, uint64_t seed_word, int64_t i_lo,
                      int64_t i_hi, int64_t shard_block, int rank, int nranks, int64_t* hits, double* zmax,
                      void* scratch, void* stream) {
@@ -843,6 +871,8 @@ int wg_run_avalanche(const double* dem, const double* dem_quad, int64_t nrows, i
   if (rc) return rc;
   if (dem_quad != nullptr && (((uintptr_t)dem_quad) & 31) != 0)
     return wg::set_error(WG_EARG, "dem_quad must be 32-byte aligned");
+  if (dem_pair != nullptr && (((uintptr_t)dem_pair) & 15) != 0)
+    return wg::set_error(WG_EARG, "dem_pair must be 16-byte aligned");
   if (per_cell < 1) return wg::set_error(WG_EARG, "particles_per_release_cell must be >= 1");
   if (nranks < 1 || rank < 0 || rank >= nranks) return wg::set_error(WG_EARG, "bad rank %d of %d", rank, nranks);
   if (shard_block < 1) return wg::set_error(WG_EARG, "shard_block must be >= 1");
@@ -851,6 +881,7 @@ int wg_run_avalanche(const double* dem, const double* dem_quad, int64_t nrows, i
     return wg::set_error(WG_EARG, "null buffer");
   World w = make_world(dem, nrows, ncols, ox, oy, cs, xmax, ymax, tana, p, omp, rscale, rh, max_steps);
   w.quad = dem_quad;
+  w.pair = dem_quad != nullptr ? nullptr : dem_pair;
   Work wk{};
   wk.cells = cells;
   wk.per_cell = per_cell;
