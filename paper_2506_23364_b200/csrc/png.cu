@@ -15,17 +15,15 @@
 //                  byte + residuals per row) and its Adler-32;
 //   lz_kernel      one warp per ~32 KiB chunk of rows: LZ77 parse with a
 //                  32-position lookahead (lane k checks position i + k; the
-//                  first match ends the step) and one-step lazy evaluation
-//                  (half the warp measures the match one byte later).
-//                  Candidates per position: the 4 most recent positions with
-//                  the same 3-byte hash (a per-chunk bucket table in global
-//                  memory, every consumed position inserted warp-parallel,
-//                  one writer per bucket so the parse is deterministic) and
-//                  the image-shaped distances 1, 4, row, 2 rows, row +- 4;
-//                  each lane measures
-//                  one candidate, the warp keeps the longest (ties: the
-//                  lowest lane); matches may reach back 32 KiB into earlier
-//                  chunks.  Tokens go to a per-chunk array;
+//                  first match ends the step), then the whole warp measures
+//                  every candidate of that position -- the kRing most recent
+//                  positions with the same 3-byte hash (per-chunk ring
+//                  buckets in global memory, every consumed position
+//                  inserted warp-parallel, deterministically) and the
+//                  image-shaped distances 1, 4, row, 2 rows, row +- 4 -- and
+//                  of the next one (one-step lazy evaluation); the longest
+//                  wins (ties: the nearer); matches may reach back 32 KiB
+//                  into earlier chunks.  Tokens go to a per-chunk array;
 //   emit_kernel    one CTA per image: symbol histograms, dynamic Huffman
 //                  codes (Moffat-Katajainen lengths limited to 15 bits,
 //                  canonical codes, run-length coded code lengths; one
@@ -228,28 +226,33 @@ struct Layout {
 };
 
 // LZ77 knobs (A/B on the 1365-tile bench, hillshade / overlay ms and mean
-// KB: base (10 hash bits, first-32 inserts, greedy) 71.7 / 114.3 ms, 40.7 /
-// 82.7 KB; + 12 hash bits, every consumed position inserted, one-step lazy
-// evaluation: 68.6 / 118.3 ms, 40.5 / 80.5 KB; + 8 slots: 74.5 / 149.3 ms,
-// 38.5 / 80.0 KB)
+// KB): see DESIGN.md section 6 (tile PNG row).
 #ifndef WG_PNG_HBITS
-#define WG_PNG_HBITS 12
-#endif
-#ifndef WG_PNG_INSERT_ALL
-#define WG_PNG_INSERT_ALL 1
+#define WG_PNG_HBITS 11
 #endif
 #ifndef WG_PNG_LAZY
 #define WG_PNG_LAZY 1
 #endif
+#ifndef WG_PNG_LAZY_MAX
+#define WG_PNG_LAZY_MAX 8  // lazy evaluation only after matches shorter than this (zlib's max_lazy)
+#endif
+#ifndef WG_PNG_RING
+#define WG_PNG_RING 16
+#endif
+#ifndef WG_PNG_QUICK
+#define WG_PNG_QUICK 4
+#endif
 constexpr int kHashBits = WG_PNG_HBITS;
 constexpr int kBuckets = 1 << kHashBits;  // per chunk
-#ifndef WG_PNG_SLOTS
-#define WG_PNG_SLOTS 4
-#endif
-// most recent positions per bucket: 4 or 8 (8: 5 % smaller hillshade tiles,
-// the runout overlay 26 % slower)
-constexpr int kSlots = WG_PNG_SLOTS;
-constexpr int kSlotVecs = kSlots / 4;  // uint4 per bucket
+// each bucket: a ring of the kRing most recent positions with that 3-byte
+// hash (+1; 0 = empty) and its head (next slot to write)
+constexpr int kRing = WG_PNG_RING;
+constexpr int kQuick = WG_PNG_QUICK;  // most recent ring entries tried by the lookahead
+constexpr int kImageCands = 6;
+constexpr int kCands = kRing + kImageCands;
+static_assert(kCands <= 32 && kQuick <= kRing, "one candidate per lane");
+constexpr bool kLazy = WG_PNG_LAZY != 0;
+constexpr int64_t kTabWords = ((int64_t)kBuckets * (kRing + 1) + 3) / 4 * 4;  // per chunk
 constexpr int kWindow = 32768;
 
 __host__ __device__ inline Layout layout_of(int64_t W, int64_t H) {
@@ -262,7 +265,7 @@ __host__ __device__ inline Layout layout_of(int64_t W, int64_t H) {
   l.f_off = 0;
   l.tok_off = up(l.nbytes + 8);  // + slack for 4-byte compares
   l.tab_off = l.tok_off + up(l.nbytes * 4);
-  l.meta_off = l.tab_off + up((int64_t)l.nchunks * kBuckets * kSlots * 4);
+  l.meta_off = l.tab_off + up((int64_t)l.nchunks * kTabWords * 4);
   l.per_image = l.meta_off + up(8 + (int64_t)l.nchunks * 4);  // adler (u32) + pad + token counts
   return l;
 }
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(kPngThreads) filter_kernel(Batch b) {
   }
   // zero the chunks' bucket tables (positions are stored + 1; 0 = empty)
   uint4* tab = reinterpret_cast<uint4*>(base + b.lay.tab_off);
-  const int64_t nt = (int64_t)b.lay.nchunks * kBuckets * kSlotVecs;
+  const int64_t nt = (int64_t)b.lay.nchunks * kTabWords / 4;
   for (int64_t i = threadIdx.x; i < nt; i += kPngThreads) tab[i] = make_uint4(0, 0, 0, 0);
   for (int k = 0; k < 8; k++)
     if (threadIdx.x == k) F[b.lay.nbytes + k] = 0;  // compare slack
@@ -366,23 +369,10 @@ __device__ __forceinline__ int match_len(const uint8_t* F, int64_t q, int64_t p,
   return len < maxl ? len : maxl;
 }
 
-constexpr int kCands = kSlots + 6;
-constexpr bool kLazy = WG_PNG_LAZY != 0;
-constexpr bool kInsertAll = WG_PNG_INSERT_ALL != 0;
-static_assert(!kLazy || kCands <= 16, "lazy evaluation uses 16 lanes per position");
-
-// candidate k (0..kCands) for position p: the bucket's slots (as of the
-// current step), then the image-shaped distances 1, 4, row, 2 rows, row +- 4
-__device__ __forceinline__ int64_t candidate(const uint8_t* F, int64_t p, int k, int64_t S, const uint4* tab,
-                                             int64_t nbytes) {
-  if (k < kSlots) {
-    if (p + 2 >= nbytes) return -1;
-    const uint4 e = tab[hash3(F, p) * kSlotVecs + (k >> 2)];
-    const int c = k & 3;
-    const uint32_t v = c == 0 ? e.x : c == 1 ? e.y : c == 2 ? e.z : e.w;
-    return (int64_t)v - 1;
-  }
-  switch (k - kSlots) {
+// image-shaped candidate k for position p: distances 1, 4, row, 2 rows,
+// row +- 4
+__device__ __forceinline__ int64_t image_cand(int64_t p, int k, int64_t S) {
+  switch (k) {
     case 0: return p - 1;
     case 1: return p - 4;
     case 2: return p - S;
@@ -392,17 +382,43 @@ __device__ __forceinline__ int64_t candidate(const uint8_t* F, int64_t p, int k,
   }
 }
 
+
 __device__ __forceinline__ bool valid_cand(int64_t q, int64_t p) { return q >= 0 && q < p && p - q <= kWindow; }
 
-// LZ77 over one chunk with a 32-position lookahead.  Phase 1: lane k
-// checks whether any candidate of position i + k shares its first 3 bytes;
-// the first such lane f ends the step (the lanes before it are literals),
-// so incompressible stretches advance 32 bytes per step.  Phase 2: lanes
-// 0..kCands-1 each extend one candidate of position i + f (4-byte
-// compares), lanes 16.. those of i + f + 1 (lazy); the longest wins (ties:
-// the earlier candidate), and a strictly longer match at i + f + 1 makes
-// i + f a literal.  Positions are inserted after each step, one writer per
-// bucket (deterministic).
+// The longest match at position pp over all candidates, one per lane: lanes
+// 0..kRing-1 the bucket's ring entries, the next kImageCands the image
+// distances.  Returns (length << 16) | (32767 - (distance - 1)) of the best
+// (ties: the nearer), 0 if none reaches 3 bytes; the same in every lane.
+__device__ __forceinline__ unsigned best_match(const uint8_t* F, int64_t pp, int64_t end, int64_t S,
+                                               const uint32_t* ring, int64_t nbytes, int lane) {
+  const int maxl = (int)(end - pp < 258 ? end - pp : 258);
+  unsigned key = 0;
+  if (maxl >= 3) {
+    int64_t q = -1;
+    if (lane < kRing) {
+      if (pp + 2 < nbytes) q = (int64_t)ring[(int64_t)hash3(F, pp) * kRing + lane] - 1;
+    } else if (lane < kCands) {
+      q = image_cand(pp, lane - kRing, S);
+    }
+    if (valid_cand(q, pp)) {
+      const int len = match_len(F, q, pp, maxl);
+      if (len >= 3) key = ((unsigned)len << 16) | (unsigned)(32767 - (pp - q - 1));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+  return key;
+}
+
+// LZ77 over one chunk with a 32-position lookahead.  Phase 1: lane k checks
+// whether the kQuick most recent same-hash positions or the image distances
+// of position i + k share its first 3 bytes; the first such lane f ends the
+// step (the lanes before it are literals), so incompressible stretches
+// advance 32 bytes per step.  Phase 2: the whole warp measures every
+// candidate of i + f (all kRing ring entries + image distances) and, lazily,
+// of i + f + 1; a strictly longer match one byte later makes i + f a literal
+// (zlib's deflate_slow rule).  Every consumed position is then inserted into
+// its bucket's ring (same-bucket lanes take consecutive slots in position
+// order; deterministic).
 __global__ void __launch_bounds__(256) lz_kernel(Batch b, int64_t nwork) {
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wid >= nwork) return;
@@ -411,7 +427,8 @@ __global__ void __launch_bounds__(256) lz_kernel(Batch b, int64_t nwork) {
   uint8_t* base = b.scratch + (int64_t)img * b.lay.per_image;
   const uint8_t* F = base + b.lay.f_off;
   uint32_t* tok = reinterpret_cast<uint32_t*>(base + b.lay.tok_off);
-  uint4* tab = reinterpret_cast<uint4*>(base + b.lay.tab_off) + (int64_t)ch * kBuckets * kSlotVecs;
+  uint32_t* ring = reinterpret_cast<uint32_t*>(base + b.lay.tab_off) + (int64_t)ch * kTabWords;
+  uint32_t* heads = ring + (int64_t)kBuckets * kRing;
   uint32_t* counts = reinterpret_cast<uint32_t*>(base + b.lay.meta_off + 8);
   const int64_t S = 4 * (int64_t)b.W + 1;
   const int64_t start = (int64_t)ch * b.lay.rows_per_chunk * S;
@@ -426,8 +443,16 @@ __global__ void __launch_bounds__(256) lz_kernel(Batch b, int64_t nwork) {
     bool quick = false;
     if (p + 3 <= end) {
       const uint32_t head = load4(F, p) & 0xFFFFFFu;
-      for (int k = 0; k < kCands && !quick; k++) {
-        const int64_t q = candidate(F, p, k, S, tab, nbytes);
+      if (p + 2 < nbytes) {
+        const uint32_t hb = hash3(F, p);
+        const uint32_t h0 = heads[hb];
+        for (int k = 1; k <= kQuick && !quick; k++) {
+          const int64_t q = (int64_t)ring[(int64_t)hb * kRing + (h0 + kRing - k) % kRing] - 1;
+          quick = valid_cand(q, p) && (load4(F, q) & 0xFFFFFFu) == head;
+        }
+      }
+      for (int k = 0; k < kImageCands && !quick; k++) {
+        const int64_t q = image_cand(p, k, S);
         quick = valid_cand(q, p) && (load4(F, q) & 0xFFFFFFu) == head;
       }
     }
@@ -438,59 +463,49 @@ __global__ void __launch_bounds__(256) lz_kernel(Batch b, int64_t nwork) {
     int64_t adv = f;
     if (hit) {
       const int64_t pf = i + f;
-      // lanes 0-15 extend the candidates of pf; with WG_PNG_LAZY lanes 16-31
-      // those of pf + 1 (one-step lazy evaluation: a longer match one byte
-      // later turns pf into a literal, as zlib's deflate_slow)
-      const int half = kLazy ? (lane >> 4) : 0;
-      const int k = kLazy ? (lane & 15) : lane;
-      const int64_t pp = pf + half;
-      const int maxl = (int)(end - pp < 258 ? end - pp : 258);
-      int len = 0;
-      int64_t q = -1;
-      if (k < kCands && maxl >= 3) {
-        q = candidate(F, pp, k, S, tab, nbytes);
-        if (valid_cand(q, pp)) len = match_len(F, q, pp, maxl);
-      }
-      unsigned best = ((unsigned)len << 8) | (unsigned)(31 - lane);
-      for (int o = kLazy ? 8 : 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-      const unsigned best0 = __shfl_sync(0xffffffffu, best, 0);
-      const unsigned best1 = kLazy ? __shfl_sync(0xffffffffu, best, 16) : 0u;
-      const bool later = kLazy && (best1 >> 8) > (best0 >> 8) && (best1 >> 8) >= 3;
-      const unsigned bw = later ? best1 : best0;
-      const int mlen = (int)(bw >> 8);
-      const int64_t mq = __shfl_sync(0xffffffffu, q, 31 - (int)(bw & 255u));
-      if (later) {
-        if (lane == 0) {
-          out[ntok + f] = F[pf];
-          out[ntok + f + 1] = ((uint32_t)mlen << 16) | (uint32_t)(pf + 1 - mq - 1);
+      const unsigned k0 = best_match(F, pf, end, S, ring, nbytes, lane);
+      const unsigned k1 =
+          (kLazy && (k0 >> 16) < WG_PNG_LAZY_MAX) ? best_match(F, pf + 1, end, S, ring, nbytes, lane) : 0u;
+      const bool later = (k1 >> 16) > (k0 >> 16);
+      const unsigned kw = later ? k1 : k0;
+      const int mlen = (int)(kw >> 16);
+      const uint32_t dm1 = 32767u - (kw & 0xFFFFu);  // distance - 1
+      if (mlen >= 3) {
+        if (later) {
+          if (lane == 0) {
+            out[ntok + f] = F[pf];
+            out[ntok + f + 1] = ((uint32_t)mlen << 16) | dm1;
+          }
+          ntok += f + 2;
+          adv += 1 + mlen;
+        } else {
+          if (lane == 0) out[ntok + f] = ((uint32_t)mlen << 16) | dm1;
+          ntok += f + 1;
+          adv += mlen;
         }
-        ntok += f + 2;
-        adv += 1 + mlen;
-      } else {
-        if (lane == 0) out[ntok + f] = ((uint32_t)mlen << 16) | (uint32_t)(pf - mq - 1);
+      } else {  // the 3-byte hit was at the chunk end: a literal
+        if (lane == 0) out[ntok + f] = F[pf];
         ntok += f + 1;
-        adv += mlen;
+        adv += 1;
       }
     } else {
       ntok += f;
     }
-    // insert the consumed positions (the first 32, or all with
-    // WG_PNG_INSERT_ALL), newest per bucket wins
-    for (int64_t b0 = 0; b0 < (kInsertAll ? adv : 1); b0 += 32) {
+    // insert every consumed position: lanes of one bucket take consecutive
+    // ring slots in position order (only the last kRing of a group land)
+    for (int64_t b0 = 0; b0 < adv; b0 += 32) {
       const int64_t pi = i + b0 + lane;
       const int nins = adv - b0 < 32 ? (int)(adv - b0) : 32;
       const bool ins = lane < nins && pi + 2 < nbytes;
-      const uint32_t h = ins ? hash3(F, pi) : 0xFFFFFFFFu - lane;
-      const unsigned grp = __match_any_sync(0xffffffffu, h);
-      if (ins && (31 - __clz(grp)) == lane) {
-        uint4* bk = tab + (int64_t)h * kSlotVecs;
-        const uint4 e = bk[0];
-        if (kSlotVecs == 2) {
-          const uint4 f = bk[1];
-          bk[1] = make_uint4(e.w, f.x, f.y, f.z);
-        }
-        bk[0] = make_uint4((uint32_t)(pi + 1), e.x, e.y, e.z);
-      }
+      const uint32_t hb = ins ? hash3(F, pi) : 0xFFFFFFFFu - lane;
+      const unsigned grp = __match_any_sync(0xffffffffu, hb);
+      const int leader = __ffs(grp) - 1;
+      const int g = __popc(grp), r = __popc(grp & ((1u << lane) - 1u));
+      uint32_t h0 = 0;
+      if (ins && lane == leader) h0 = heads[hb];
+      h0 = __shfl_sync(0xffffffffu, h0, leader);
+      if (ins && g - r <= kRing) ring[(int64_t)hb * kRing + (h0 + r) % kRing] = (uint32_t)(pi + 1);
+      if (ins && lane == leader) heads[hb] = (h0 + g) % kRing;
       __syncwarp();
     }
     i += adv;
