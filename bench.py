@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--config", choices=["c3", "c5"], default="c3",
                     help="c3: 16384^2 stride 32 (default, BASELINE configs[2]); "
-                         "c5: 65536^2 stride 128 seed 2 (configs[4]; slope-only prefix, no e2e/CPU legs)")
+                         "c5: 65536^2 stride 128 seed 2 (configs[4]; lattice-slope mask prefix, no e2e/CPU legs)")
     ap.add_argument("--overlay-size", type=int, default=8192)
     a = ap.parse_args()
     a.slope_only = False
@@ -77,7 +77,7 @@ def parse():
 
 
 def workload(a) -> dict:
-    which = "configs[4], slope-only prefix" if a.config == "c5" else "configs[2]"
+    which = "configs[4], mask from the slope at lattice cells" if a.config == "c5" else "configs[2]"
     gib = a.size * a.size * 8 / 2**30
     return {
         "workload": f"avalanche release points + trajectories, synthetic {a.size}x{a.size} DEM (BASELINE {which})",
@@ -227,9 +227,9 @@ def main() -> None:
     import paper_2506_23364_b200 as wf
     from paper_2506_23364_b200 import _lib
     from paper_2506_23364_b200.shard import merge_runout, release_cells_banded
-    from paper_2506_23364_b200.simulate import release_cells, run_avalanche_device
+    from paper_2506_23364_b200.simulate import release_cells, release_mask_from_dem, run_avalanche_device
     from paper_2506_23364_b200.synth import synth_dem_device
-    from paper_2506_23364_b200.terrain import compute_normals_and_slope, compute_slope
+    from paper_2506_23364_b200.terrain import compute_normals_and_slope
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -263,12 +263,12 @@ def main() -> None:
             # upstream nodes sharded by row band, cell lists all-gathered
             cells = release_cells_banded(g, 30.0, 45.0, a.stride, rank, world, with_normals=not a.slope_only)
         else:
-            if a.slope_only:
-                slope = compute_slope(g)
+            if a.slope_only:  # C5: the slope only where the mask can be set
+                mask = release_mask_from_dem(g, 30.0, 45.0, a.stride)
             else:
                 _, slope = compute_normals_and_slope(g)
-            mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
-            del slope
+                mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
+                del slope
             cells = release_cells(mask)
         hits = torch.zeros((g.nrows, g.ncols), dtype=torch.int64, device=dev)
         zmax = torch.zeros((g.nrows, g.ncols), dtype=torch.float64, device=dev)

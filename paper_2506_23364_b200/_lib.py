@@ -44,6 +44,8 @@ SIGNATURES: dict[str, tuple] = {
     "wg_hillshade": (c_int, [c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_ptr, c_ptr]),
     "wg_hillshade_rgba": (c_int, [c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_ptr, c_ptr]),
     "wg_release_mask": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_i64, c_ptr, c_ptr]),
+    "wg_lattice_release_mask": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_i64, c_i64, c_i64, c_ptr,
+                                        c_ptr]),
     "wg_compact_scratch_bytes": (c_size, [c_i64]),
     "wg_mask_compact": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "wg_avalanche_scratch_bytes": (c_size, [c_i64, c_i64, c_i64]),

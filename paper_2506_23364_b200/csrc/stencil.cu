@@ -59,6 +59,42 @@ __device__ __forceinline__ double slope_of(double nz) {
   return WG_MUL(acos(c), 57.29577951308232);
 }
 
+// The unit normal of cell (i, j) from its own height and its four
+// neighbours' (terrain.py:69-96): central differences inside, one-sided on
+// the borders (terrain.py:79-88; neighbours beyond a border are not read),
+// five divisions through shared reciprocals with one guard for all of them
+// -- the rare guard miss recomputes the cell with __ddiv_rn.  Shared by the
+// normals pass and the lattice mask so both give the same bits.
+__device__ __forceinline__ void cell_normal(double cur, double west, double east, double up, double dn, int i, int jc,
+                                            int nrows, int ncols, double cs, double two_cs, double rcs, double r2cs,
+                                            bool cs_ok, double& n0, double& n1, double& nz) {
+  const bool xb = (jc == 0) | (jc == ncols - 1), yb = (i == 0) | (i == nrows - 1);
+  const double xa = WG_SUB(jc == 0 ? east : (jc == ncols - 1 ? cur : east),
+                           jc == 0 ? cur : (jc == ncols - 1 ? west : west));
+  const double ya = WG_SUB(i == 0 ? cur : up, i == 0 ? dn : (i == nrows - 1 ? cur : dn));
+  const double xd = xb ? cs : two_cs, xr = xb ? rcs : r2cs;
+  const double yd = yb ? cs : two_cs, yr = yb ? rcs : r2cs;
+  bool ok = cs_ok;
+  double dzdx = div_fast(xa, xd, xr, ok), dzdy = div_fast(ya, yd, yr, ok);
+  double nx = -dzdx, ny = -dzdy;
+  double len = WG_SQRT(WG_ADD(WG_ADD(WG_MUL(nx, nx), WG_MUL(ny, ny)), 1.0));
+  const double rl = rcp_refined(len);
+  ok = ok && b_ok(len);
+  n0 = div_fast(nx, len, rl, ok);
+  n1 = div_fast(ny, len, rl, ok);
+  nz = div_fast(1.0, len, rl, ok);
+  if (!ok) {
+    dzdx = __ddiv_rn(xa, xd);
+    dzdy = __ddiv_rn(ya, yd);
+    nx = -dzdx;
+    ny = -dzdy;
+    len = WG_SQRT(WG_ADD(WG_ADD(WG_MUL(nx, nx), WG_MUL(ny, ny)), 1.0));
+    n0 = __ddiv_rn(nx, len);
+    n1 = __ddiv_rn(ny, len);
+    nz = __ddiv_rn(1.0, len);
+  }
+}
+
 // 2.5-D stencil: a thread owns one column of a band of kNormBand rows and
 // walks down it with a rolling (north, centre, south) register window, so
 // every DEM value is loaded once per band (+2 halo rows); east/west
@@ -100,34 +136,8 @@ __global__ void __launch_bounds__(kNormThreads, WG_NORM_MINB) normals_kernel(con
     const double* row = e + (size_t)i * ncols;
     if (lane == 0 && jc > 0) west = __ldg(row + jc - 1);
     if ((lane == 31 || j + 1 >= ncols) && jc + 1 < ncols) east = __ldg(row + jc + 1);
-    // central differences inside, one-sided on the borders (terrain.py:79-88)
-    const bool xb = (jc == 0) | (jc == ncols - 1), yb = (i == 0) | (i == nrows - 1);
-    const double xa = WG_SUB(jc == 0 ? east : (jc == ncols - 1 ? cur : east),
-                             jc == 0 ? cur : (jc == ncols - 1 ? west : west));
-    const double ya = WG_SUB(i == 0 ? cur : up, i == 0 ? dn : (i == nrows - 1 ? cur : dn));
-    const double xd = xb ? cs : two_cs, xr = xb ? rcs : r2cs;
-    const double yd = yb ? cs : two_cs, yr = yb ? rcs : r2cs;
-    // five divisions through shared reciprocals, one guard for all of them;
-    // the rare guard miss recomputes the cell with __ddiv_rn
-    bool ok = cs_fast && c2_fast;
-    double dzdx = div_fast(xa, xd, xr, ok), dzdy = div_fast(ya, yd, yr, ok);
-    double nx = -dzdx, ny = -dzdy;
-    double len = WG_SQRT(WG_ADD(WG_ADD(WG_MUL(nx, nx), WG_MUL(ny, ny)), 1.0));
-    const double rl = rcp_refined(len);
-    ok = ok && b_ok(len);
-    double n0 = div_fast(nx, len, rl, ok);
-    double n1 = div_fast(ny, len, rl, ok);
-    double nz = div_fast(1.0, len, rl, ok);
-    if (!ok) {
-      dzdx = __ddiv_rn(xa, xd);
-      dzdy = __ddiv_rn(ya, yd);
-      nx = -dzdx;
-      ny = -dzdy;
-      len = WG_SQRT(WG_ADD(WG_ADD(WG_MUL(nx, nx), WG_MUL(ny, ny)), 1.0));
-      n0 = __ddiv_rn(nx, len);
-      n1 = __ddiv_rn(ny, len);
-      nz = __ddiv_rn(1.0, len);
-    }
+    double n0, n1, nz;
+    cell_normal(cur, west, east, up, dn, i, jc, nrows, ncols, cs, two_cs, rcs, r2cs, cs_fast && c2_fast, n0, n1, nz);
     const size_t cell = (size_t)i * ncols + j;
     if (slope != nullptr && live) slope[cell] = slope_of(nz);
     if (nrm != nullptr) {
@@ -218,6 +228,30 @@ __global__ void release_mask_kernel(const double* __restrict__ s, int nrows, int
     } else {
       for (int q = 0; q < 16 && c0 + q < ncols; q++) out[q] = v[q];
     }
+  }
+}
+
+// Release mask straight from the DEM for grids whose slope field is not
+// otherwise needed (C5): the slope is computed only at stride-lattice cells
+// of rows [row0, row1) (the only cells the mask can set), with the normals
+// pass's own per-cell arithmetic, so the mask equals
+// detect_release_points(steepness_deg(compute_normals(grid))) bit for bit.
+// Other mask bytes are zeroed by the caller.
+__global__ void lattice_mask_kernel(const double* __restrict__ e, int nrows, int ncols, double cs, double two_cs,
+                                    double lo, double hi, int stride, int row0, int row1, uint8_t* __restrict__ mask) {
+  const int64_t lr = (row1 - row0 + stride - 1) / stride, lc = (ncols + stride - 1) / stride;
+  const double rcs = rcp_refined(cs), r2cs = rcp_refined(two_cs);
+  const bool cs_ok = b_ok(cs) && b_ok(two_cs);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < lr * lc; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = row0 + (int)(t / lc) * stride, j = (int)(t % lc) * stride;
+    const double* c = e + (size_t)i * ncols + j;
+    const double cur = __ldg(c);
+    const double west = j > 0 ? __ldg(c - 1) : 0.0, east = j + 1 < ncols ? __ldg(c + 1) : 0.0;
+    const double up = i > 0 ? __ldg(c - ncols) : 0.0, dn = i + 1 < nrows ? __ldg(c + ncols) : 0.0;
+    double n0, n1, nz;
+    cell_normal(cur, west, east, up, dn, i, j, nrows, ncols, cs, two_cs, rcs, r2cs, cs_ok, n0, n1, nz);
+    const double x = slope_of(nz);
+    mask[(size_t)(i - row0) * ncols + j] = (uint8_t)((x >= lo) & (x <= hi));
   }
 }
 
@@ -444,6 +478,24 @@ int wg_release_mask(const double* slope, int64_t nrows, int64_t ncols, double lo
   const dim3 grid((unsigned)((ncols + 16 * kBlock - 1) / (16 * kBlock)), (unsigned)(nrows < 8192 ? nrows : 8192));
   release_mask_kernel<<<grid, kBlock, 0, wg::as_stream(stream)>>>(slope, (int)nrows, (int)ncols, lo, hi, st, mask);
   WG_LAUNCH_CHECK("release_mask_kernel");
+  return WG_OK;
+}
+
+int wg_lattice_release_mask(const double* elev, int64_t nrows, int64_t ncols, double cs, double two_cs, double lo,
+                            double hi, int64_t stride, int64_t row0, int64_t row1, uint8_t* mask, void* stream) {
+  if (stride < 1) return wg::set_error(WG_EARG, "stride must be >= 1, got %lld", (long long)stride);
+  if (nrows < 2 || ncols < 2) return wg::set_error(WG_EARG, "grid must be at least 2x2");
+  if (row0 < 0 || row1 < row0 || row1 > nrows) return wg::set_error(WG_EARG, "bad row range");
+  if (nrows > 0x7fffffff || ncols > 0x7fffffff) return wg::set_error(WG_EARG, "grid too large");
+  if (row1 == row0) return WG_OK;
+  if (!elev || !mask) return wg::set_error(WG_EARG, "null buffer");
+  cudaStream_t st = wg::as_stream(stream);
+  WG_CUDA_TRY(cudaMemsetAsync(mask, 0, (size_t)(row1 - row0) * (size_t)ncols, st));
+  const int64_t s = stride > nrows + ncols ? nrows + ncols : stride;  // larger strides: same lattice
+  const int64_t cells = ((row1 - row0 + s - 1) / s) * ((ncols + s - 1) / s);
+  lattice_mask_kernel<<<wg::resident_grid(lattice_mask_kernel, cells, kBlock), kBlock, 0, st>>>(
+      elev, (int)nrows, (int)ncols, cs, two_cs, lo, hi, (int)s, (int)row0, (int)row1, mask);
+  WG_LAUNCH_CHECK("lattice_mask_kernel");
   return WG_OK;
 }
 

@@ -86,15 +86,20 @@ def release_cells_banded(grid, min_deg: float, max_deg: float, stride: int, rank
     if r1 > r0:
         a, b = max(r0 - 1, 0), min(r1 + 1, H)
         sub = e[a:b]
-        slope = _device.empty((b - a, W), torch.float64)
-        nrm = _device.empty((b - a, W, 3), torch.float64) if with_normals else None
         cs = grid.cellsize
-        _lib.check(L.wg_normals(_lib.ptr(sub), b - a, W, cs, 2.0 * cs, _lib.ptr(nrm), _lib.ptr(slope),
-                                _lib.stream_ptr()), TerrainError)
-        band = slope[r0 - a : r1 - a]
         mask = _device.empty((r1 - r0, W), torch.uint8)
-        _lib.check(L.wg_release_mask(_lib.ptr(band), r1 - r0, W, float(min_deg), float(max_deg), int(stride),
-                                     _lib.ptr(mask), _lib.stream_ptr()))
+        if with_normals:
+            slope = _device.empty((b - a, W), torch.float64)
+            nrm = _device.empty((b - a, W, 3), torch.float64)
+            _lib.check(L.wg_normals(_lib.ptr(sub), b - a, W, cs, 2.0 * cs, _lib.ptr(nrm), _lib.ptr(slope),
+                                    _lib.stream_ptr()), TerrainError)
+            band = slope[r0 - a : r1 - a]
+            _lib.check(L.wg_release_mask(_lib.ptr(band), r1 - r0, W, float(min_deg), float(max_deg), int(stride),
+                                         _lib.ptr(mask), _lib.stream_ptr()))
+        else:  # the slope at lattice cells only, straight from the band + halo rows
+            _lib.check(L.wg_lattice_release_mask(_lib.ptr(sub), b - a, W, cs, 2.0 * cs, float(min_deg),
+                                                 float(max_deg), int(stride), r0 - a, r1 - a, _lib.ptr(mask),
+                                                 _lib.stream_ptr()), TerrainError)
         n = mask.numel()
         cells = _device.empty((max(n, 1),), torch.int64)
         count = _device.zeros((1,), torch.int64)
