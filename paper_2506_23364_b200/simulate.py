@@ -367,19 +367,28 @@ def _world() -> tuple[int, int]:
     return 0, 1
 
 
-_LAYOUT_HEADROOM = 4 << 30  # free HBM kept for scratch after a gather layout
+def _try_empty(n: int) -> torch.Tensor | None:
+    """A transient float64 buffer, or None when HBM cannot hold it (the
+    allocation attempt is the fit test: cheaper than querying the driver's
+    free memory on every launch, and the buffer is released to the caching
+    allocator as soon as the trajectory launch is queued)."""
+    dev = _device.device()
+    if 8 * n > torch.cuda.get_device_properties(dev).total_memory - torch.cuda.memory_allocated(dev):
+        return None  # cannot fit: skip the attempt (a failed one flushes the allocator's cache)
+    try:
+        return _device.empty((n,), torch.float64)
+    except torch.cuda.OutOfMemoryError:
+        return None
 
 
 def build_quad(grid: DemGrid) -> torch.Tensor | None:
     """Patch-corner layout of the DEM (wg_build_quad: 32 B per cell, four
     times the DEM) so every particle step gathers its bilinear patch with one
-    256-bit load; None when it would not fit (see build_gather_layout)."""
-    need = grid.nrows * grid.ncols * 32
-    free, _ = torch.cuda.mem_get_info()
-    if need > free - _LAYOUT_HEADROOM:
+    256-bit load; None when it does not fit (see build_gather_layout)."""
+    quad = _try_empty(grid.nrows * grid.ncols * 4)
+    if quad is None:
         return None
     L = _lib.lib()
-    quad = _device.empty((grid.nrows * grid.ncols * 4,), torch.float64)
     _lib.check(L.wg_build_quad(_lib.ptr(grid.device_elevations()), grid.nrows, grid.ncols, _lib.ptr(quad),
                                _lib.stream_ptr()), ParamError)
     return quad
@@ -387,13 +396,11 @@ def build_quad(grid: DemGrid) -> torch.Tensor | None:
 
 def build_pair(grid: DemGrid) -> torch.Tensor | None:
     """Row-pair layout of the DEM (wg_build_pair: 16 B per cell, twice the
-    DEM): two 128-bit loads per step; None when it would not fit."""
-    need = grid.nrows * grid.ncols * 16
-    free, _ = torch.cuda.mem_get_info()
-    if need > free - _LAYOUT_HEADROOM:
+    DEM): two 128-bit loads per step; None when it does not fit."""
+    pair = _try_empty(grid.nrows * grid.ncols * 2)
+    if pair is None:
         return None
     L = _lib.lib()
-    pair = _device.empty((grid.nrows * grid.ncols * 2,), torch.float64)
     _lib.check(L.wg_build_pair(_lib.ptr(grid.device_elevations()), grid.nrows, grid.ncols, _lib.ptr(pair),
                                _lib.stream_ptr()), ParamError)
     return pair
