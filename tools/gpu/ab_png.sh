@@ -1,6 +1,6 @@
 # A/B of PNG encoder compile variants (BUILDS = NVCC_EXTRA values) on the tile bench
 # (a variant may hold several flags separated by commas)
-for v in ${BUILDS:-"-DWG_PNG_SLOTS=4" "-DWG_PNG_SLOTS=8"}; do
+for v in ${BUILDS:-"-DWG_PNG_RING=16" "-DWG_PNG_RING=26"}; do
   make -C paper_2506_23364_b200/csrc clean >/dev/null
   make -C paper_2506_23364_b200/csrc -j8 NVCC_EXTRA="${v//,/ }" >/dev/null 2>&1 || { echo "build $v failed"; continue; }
   timeout 600 python -m pytest tests/test_gpu_tiles.py -x -q > gpurun_out/pt.log 2>&1 || { echo "$v tests FAILED"; tail -5 gpurun_out/pt.log; }
