@@ -13,7 +13,7 @@ kname = sys.argv[2] if len(sys.argv) > 2 else "traj_kernel"
 
 
 def ncu(*args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, "-k", f"regex:{kname}", *args], capture_output=True, text=True).stdout
 
 
 r = list(csv.reader(io.StringIO(ncu("--page", "details", "--csv"))))
