@@ -56,16 +56,20 @@ def gpu_encode(pyr, L, tile_px=256):
         best = min(best, e0.elapsed_time(e1))
     total = sum(int(b[2].sum()) for b in bufs.values())
     del bufs
-    # end to end through the public API (bytes on the host)
-    t0 = time.perf_counter()
-    n = 0
-    nbytes = 0
-    for z in range(zmax + 1):
-        pngs = wf.tile_pngs(pyr, z)
-        n += len(pngs)
-        nbytes += sum(len(v) for v in pngs.values())
-    e2e = (time.perf_counter() - t0) * 1e3
-    return best, e2e, nbytes, n, total
+    # end to end through the public API (bytes on the host); a tile server
+    # calls it repeatedly: steady state = best of 3 (the first call also
+    # allocates the encoder's buffers and the pinned staging ring)
+    runs = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        n = 0
+        nbytes = 0
+        for z in range(zmax + 1):
+            pngs = wf.tile_pngs(pyr, z)
+            n += len(pngs)
+            nbytes += sum(len(v) for v in pngs.values())
+        runs.append((time.perf_counter() - t0) * 1e3)
+    return best, min(runs), nbytes, n, total, runs[0]
 
 
 def cpu_encode(pyr, sample, tile_px=256):
@@ -104,10 +108,11 @@ def main():
         "workload": "all 256-px tiles, zooms 0-5 (1365 per pyramid) of two 8192^2 pyramids: hillshade of "
                     "synth_dem(8192, 1) and the stock avalanche overlay (stride 16, 256 particles/cell)"}}
     for name, pyr in (("hillshade", hs), ("overlay", ov)):
-        k_ms, e2e_ms, nbytes, ntiles, _ = gpu_encode(pyr, L)
+        k_ms, e2e_ms, nbytes, ntiles, _, e2e_first = gpu_encode(pyr, L)
         cpu_s, cpu_bytes, cpu_n = cpu_encode(pyr, a.sample)
         out[name] = {"tiles": ntiles, "kernel_ms": k_ms, "value": ntiles / (k_ms / 1e3), "e2e_ms": e2e_ms,
-                     "e2e_value": ntiles / (e2e_ms / 1e3), "mean_png_bytes": nbytes / ntiles,
+                     "e2e_value": ntiles / (e2e_ms / 1e3), "e2e_first_call_ms": e2e_first,
+                     "mean_png_bytes": nbytes / ntiles,
                      "cpu_baseline": {"kind": "reference path (numpy slice + Pillow PNG)", "cores": 1,
                                       "sample": f"{cpu_n} evenly spaced tiles of the same pyramid",
                                       "value": cpu_n / cpu_s, "unit": "tiles/s",
