@@ -33,7 +33,7 @@ def wrap(mod, name):
 
 from paper_2506_23364_b200 import _device  # noqa: E402
 
-for mod, name in ((torch.cuda, "mem_get_info"), (_device, "empty"), (simulate, "build_quad"), (workflow, "run_avalanche"), (workflow, "colorize"), (workflow, "build_mipmap"),
+for mod, name in ((simulate, "_try_empty"), (_device, "empty"), (simulate, "build_quad"), (workflow, "run_avalanche"), (workflow, "colorize"), (workflow, "build_mipmap"),
                   (workflow, "avalanche_stats"), (simulate, "release_cells"), (simulate, "build_gather_layout"),
                   (simulate, "run_avalanche_device")):
     if hasattr(mod, name):
