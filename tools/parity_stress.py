@@ -2,16 +2,21 @@
 shapes 20-300, cellsizes 0.5-100, origins up to 1e6, terraced terrain every 7th case,
 random release sets and parameters).  usage: python tools/parity_stress.py"""
 import sys
-
-import numpy as np
 from pathlib import Path
 
+import numpy as np
+
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import paper_2506_23364_b200 as wf
-from oracle import traj
-from paper_2506_23364_b200.simulate import particle_records
-from paper_2506_23364_b200.synth import synth_dem_host
-bits = lambda a: np.ascontiguousarray(a).view(np.int64)
+import paper_2506_23364_b200 as wf  # noqa: E402
+from oracle import traj  # noqa: E402
+from paper_2506_23364_b200.synth import synth_dem_host  # noqa: E402
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.int64)
+
+
+
 bad = 0
 for case in range(100, 160):
     r = np.random.default_rng(1000 + case)
