@@ -43,17 +43,22 @@ SIGNATURES: dict[str, tuple] = {
     "wg_steepness": (c_int, [c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_hillshade": (c_int, [c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_ptr, c_ptr]),
     "wg_hillshade_rgba": (c_int, [c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_ptr, c_ptr]),
-    "wg_release_mask": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_i64, c_ptr, c_ptr]),
+    "wg_release_mask": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_lattice_release_mask": (c_int, [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_i64, c_i64, c_i64, c_ptr,
-                                        c_ptr]),
+                                        c_ptr, c_ptr]),
     "wg_compact_scratch_bytes": (c_size, [c_i64]),
     "wg_mask_compact": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "wg_avalanche_scratch_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "wg_run_avalanche": (
         c_int,
         [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl,
-         c_i64, c_ptr, c_i64, c_u64, c_i64, c_i64, c_i64, c_int, c_int, c_ptr, c_ptr, c_ptr, c_ptr],
+         c_i64, c_ptr, c_i64, c_u64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_int, c_ptr, c_ptr],
     ),
+    "wg_absmax": (c_int, [c_ptr, c_i64, c_ptr, c_ptr]),
+    "wg_sorted_offsets": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
+    "wg_tiles_pack": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_int, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
+    "wg_tiles_accumulate": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_int, c_ptr, c_i64, c_ptr, c_ptr]),
+    "wg_tiles_zero": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_int, c_ptr, c_i64, c_ptr]),
     "wg_build_quad": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
     "wg_build_pair": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
     "wg_trace_particle": (
@@ -69,6 +74,7 @@ SIGNATURES: dict[str, tuple] = {
     "wg_trig_eval": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_div_eval": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_sqrt_eval": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
+    "wg_acos_eval": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
     "wg_runout_stats": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_snow": (c_int, [c_ptr, c_ptr, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_int, c_dbl, c_ptr, c_ptr]),
     "wg_colorize": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr]),

@@ -184,9 +184,8 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
         raise AsciiGridError(f"invalid elevation value {data[bad_off:end].decode('ascii')!r}", line=line, column=col)
     del t, scratch
     try:
-        return DemGrid(ncols=ncols, nrows=nrows, origin_x=header["xllcorner"], origin_y=header["yllcorner"],
-                       cellsize=header["cellsize"], nodata=header["nodata_value"],
-                       elevations=values.view(nrows, ncols))
+        return DemGrid.adopt(ncols, nrows, header["xllcorner"], header["yllcorner"], header["cellsize"],
+                             header["nodata_value"], values.view(nrows, ncols))
     except GridError as exc:
         raise AsciiGridError(str(exc)) from exc
 

@@ -13,6 +13,7 @@
 #include "wg_internal.cuh"
 #include "wg_div.cuh"
 #include "wg_fp64.h"
+#include "wg_acos.h"
 
 namespace {
 
@@ -53,10 +54,30 @@ __global__ void copy2d_kernel(const double* __restrict__ src, int64_t src_ld, do
 }
 
 // ---------------------------------------------------------------- normals
-// degrees(arccos(clip(nz, -1, 1))); np.degrees multiplies by 180/pi.
+// degrees(arccos(clip(nz, -1, 1))) (terrain.py:101-102): numpy's arccos bit
+// for bit (wg_acos.h), np.degrees multiplies by 180/pi.
 __device__ __forceinline__ double slope_of(double nz) {
   const double c = wg_min(wg_max(nz, -1.0), 1.0);
-  return WG_MUL(acos(c), 57.29577951308232);
+  return WG_MUL(wg_acos(c), 57.29577951308232);
+}
+
+// Release-mask guard band: lattice cells whose slope
+// lies within kGuardDeg of a band edge are counted, so a caller can see when
+// a threshold decision rests on the last bits of the slope.  The mask kernels
+// accumulate counts[0] = set cells (ReleaseMask.count without another pass)
+// and counts[1] = borderline cells.
+constexpr double kGuardDeg = 1e-9;
+__device__ __forceinline__ unsigned borderline(double x, double lo, double hi) {
+  return (unsigned)((fabs(x - lo) < kGuardDeg) | (fabs(x - hi) < kGuardDeg));
+}
+
+__device__ __forceinline__ void add_counts(unsigned long long* counts, unsigned set, unsigned near) {
+  set = __reduce_add_sync(0xffffffffu, set);
+  near = __reduce_add_sync(0xffffffffu, near);
+  if ((threadIdx.x & 31) == 0) {
+    if (set) atomicAdd(counts, (unsigned long long)set);
+    if (near) atomicAdd(counts + 1, (unsigned long long)near);
+  }
 }
 
 // The unit normal of cell (i, j) from its own height and its four
@@ -166,6 +187,15 @@ __global__ void __launch_bounds__(kNormThreads, WG_NORM_MINB) normals_kernel(con
   }
 }
 
+__global__ void acos_eval_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ a,
+                                 double* __restrict__ d) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = __ldg(x + t);
+    if (a != nullptr) a[t] = wg_acos(v);
+    if (d != nullptr) d[t] = slope_of(v);
+  }
+}
+
 __global__ void steepness_kernel(const double* __restrict__ nrm, int64_t n, double* __restrict__ slope) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     slope[t] = slope_of(__ldg(nrm + 3 * t + 2));
@@ -201,10 +231,10 @@ __global__ void hillshade_rgba_kernel(const double* __restrict__ nrm, int64_t n,
 // the slope is read only at stride-lattice cells, the only cells the mask can
 // set (simulate.py:222-225), so for stride > 1 the pass is write-bound.
 __global__ void release_mask_kernel(const double* __restrict__ s, int nrows, int ncols, double lo, double hi,
-                                    int stride, uint8_t* __restrict__ mask) {
+                                    int stride, uint8_t* __restrict__ mask, unsigned long long* __restrict__ counts) {
   const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
-  if (c0 >= ncols) return;
-  for (int i = blockIdx.y; i < nrows; i += gridDim.y) {
+  unsigned set = 0, near = 0;
+  for (int i = blockIdx.y; c0 < ncols && i < nrows; i += gridDim.y) {
     const size_t rowoff = (size_t)i * ncols;
     unsigned char v[16];
     const bool lat_row = (i % stride) == 0;
@@ -215,6 +245,8 @@ __global__ void release_mask_kernel(const double* __restrict__ s, int nrows, int
       for (; c < c0 + 16 && c < ncols; c += stride) {
         const double x = __ldg(s + rowoff + c);
         v[c - c0] = (unsigned char)((x >= lo) & (x <= hi));
+        set += v[c - c0];
+        near += borderline(x, lo, hi);
       }
     }
     uint8_t* out = mask + rowoff + c0;
@@ -229,6 +261,7 @@ __global__ void release_mask_kernel(const double* __restrict__ s, int nrows, int
       for (int q = 0; q < 16 && c0 + q < ncols; q++) out[q] = v[q];
     }
   }
+  if (counts != nullptr) add_counts(counts, set, near);
 }
 
 // Release mask straight from the DEM for grids whose slope field is not
@@ -238,10 +271,12 @@ __global__ void release_mask_kernel(const double* __restrict__ s, int nrows, int
 // detect_release_points(steepness_deg(compute_normals(grid))) bit for bit.
 // Other mask bytes are zeroed by the caller.
 __global__ void lattice_mask_kernel(const double* __restrict__ e, int nrows, int ncols, double cs, double two_cs,
-                                    double lo, double hi, int stride, int row0, int row1, uint8_t* __restrict__ mask) {
+                                    double lo, double hi, int stride, int row0, int row1, uint8_t* __restrict__ mask,
+                                    unsigned long long* __restrict__ counts) {
   const int64_t lr = (row1 - row0 + stride - 1) / stride, lc = (ncols + stride - 1) / stride;
   const double rcs = rcp_refined(cs), r2cs = rcp_refined(two_cs);
   const bool cs_ok = b_ok(cs) && b_ok(two_cs);
+  unsigned set = 0, near = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < lr * lc; t += (int64_t)gridDim.x * blockDim.x) {
     const int i = row0 + (int)(t / lc) * stride, j = (int)(t % lc) * stride;
     const double* c = e + (size_t)i * ncols + j;
@@ -251,8 +286,12 @@ __global__ void lattice_mask_kernel(const double* __restrict__ e, int nrows, int
     double n0, n1, nz;
     cell_normal(cur, west, east, up, dn, i, j, nrows, ncols, cs, two_cs, rcs, r2cs, cs_ok, n0, n1, nz);
     const double x = slope_of(nz);
-    mask[(size_t)(i - row0) * ncols + j] = (uint8_t)((x >= lo) & (x <= hi));
+    const unsigned in = (unsigned)((x >= lo) & (x <= hi));
+    mask[(size_t)(i - row0) * ncols + j] = (uint8_t)in;
+    set += in;
+    near += borderline(x, lo, hi);
   }
+  if (counts != nullptr) add_counts(counts, set, near);
 }
 
 // ---------------------------------------------------------------- compaction
@@ -450,6 +489,14 @@ int wg_steepness(const double* normals, int64_t n, double* slope, void* stream) 
   return WG_OK;
 }
 
+int wg_acos_eval(const double* x, int64_t n, double* a, double* d, void* stream) {
+  if (n <= 0) return WG_OK;
+  if (!x || (!a && !d)) return wg::set_error(WG_EARG, "null buffer");
+  acos_eval_kernel<<<wg::resident_grid(acos_eval_kernel, n, kBlock), kBlock, 0, wg::as_stream(stream)>>>(x, n, a, d);
+  WG_LAUNCH_CHECK("acos_eval_kernel");
+  return WG_OK;
+}
+
 int wg_hillshade(const double* normals, int64_t n, double lx, double ly, double lz, uint8_t* out, void* stream) {
   if (n <= 0) return WG_OK;
   if (!normals || !out) return wg::set_error(WG_EARG, "null buffer");
@@ -469,20 +516,22 @@ int wg_hillshade_rgba(const double* normals, int64_t n, double lx, double ly, do
 }
 
 int wg_release_mask(const double* slope, int64_t nrows, int64_t ncols, double lo, double hi, int64_t stride,
-                    uint8_t* mask, void* stream) {
+                    uint8_t* mask, uint64_t* counts, void* stream) {
   if (stride < 1) return wg::set_error(WG_EARG, "stride must be >= 1, got %lld", (long long)stride);
   if (nrows * ncols <= 0) return WG_OK;
   if (!slope || !mask) return wg::set_error(WG_EARG, "null buffer");
   if (nrows > 0x7fffffff || ncols > 0x7fffffff) return wg::set_error(WG_EARG, "grid too large");
   const int st = stride > ncols + nrows ? (int)(ncols + nrows) : (int)stride;  // larger strides: same lattice
   const dim3 grid((unsigned)((ncols + 16 * kBlock - 1) / (16 * kBlock)), (unsigned)(nrows < 8192 ? nrows : 8192));
-  release_mask_kernel<<<grid, kBlock, 0, wg::as_stream(stream)>>>(slope, (int)nrows, (int)ncols, lo, hi, st, mask);
+  release_mask_kernel<<<grid, kBlock, 0, wg::as_stream(stream)>>>(slope, (int)nrows, (int)ncols, lo, hi, st, mask,
+                                                                  reinterpret_cast<unsigned long long*>(counts));
   WG_LAUNCH_CHECK("release_mask_kernel");
   return WG_OK;
 }
 
 int wg_lattice_release_mask(const double* elev, int64_t nrows, int64_t ncols, double cs, double two_cs, double lo,
-                            double hi, int64_t stride, int64_t row0, int64_t row1, uint8_t* mask, void* stream) {
+                            double hi, int64_t stride, int64_t row0, int64_t row1, uint8_t* mask, uint64_t* counts,
+                            void* stream) {
   if (stride < 1) return wg::set_error(WG_EARG, "stride must be >= 1, got %lld", (long long)stride);
   if (nrows < 2 || ncols < 2) return wg::set_error(WG_EARG, "grid must be at least 2x2");
   if (row0 < 0 || row1 < row0 || row1 > nrows) return wg::set_error(WG_EARG, "bad row range");
@@ -494,7 +543,8 @@ int wg_lattice_release_mask(const double* elev, int64_t nrows, int64_t ncols, do
   const int64_t s = stride > nrows + ncols ? nrows + ncols : stride;  // larger strides: same lattice
   const int64_t cells = ((row1 - row0 + s - 1) / s) * ((ncols + s - 1) / s);
   lattice_mask_kernel<<<wg::resident_grid(lattice_mask_kernel, cells, kBlock), kBlock, 0, st>>>(
-      elev, (int)nrows, (int)ncols, cs, two_cs, lo, hi, (int)s, (int)row0, (int)row1, mask);
+      elev, (int)nrows, (int)ncols, cs, two_cs, lo, hi, (int)s, (int)row0, (int)row1, mask,
+      reinterpret_cast<unsigned long long*>(counts));
   WG_LAUNCH_CHECK("lattice_mask_kernel");
   return WG_OK;
 }

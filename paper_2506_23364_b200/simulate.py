@@ -6,16 +6,16 @@ the reference's types, parameter validation, error behaviour and host-side
 scalar derivations (simulate.py:292-298), which are computed here with Python
 floats exactly as the reference does and handed to the kernel verbatim.
 
-Multi-GPU: when ``torch.distributed`` is initialised with world size > 1,
-run_avalanche shards the particle index space by release-point blocks across
-ranks (blocked-cyclic), each rank accumulates its private hit / drop rasters,
-and one all-reduce (int64 SUM, float64 MAX) over NCCL merges them; both merges
-are exact and commutative, so every rank holds the bitwise-identical raster a
-single GPU (and the reference) produces.
+Multi-GPU (opt-in): ``run_avalanche(..., group=pg)`` shards the particles
+by release-row bands over the ranks of the process group and merges the
+private rasters tile-sparsely (shard.py); every rank then holds the
+bitwise-identical raster a single GPU (and the reference) produces.  Without
+``group`` the call is local, as the reference's is.
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, replace
 from enum import Enum
@@ -29,7 +29,6 @@ from .grid import DemGrid
 from .overlay import OverlayTexture
 from .terrain import NormalField, SlopeField, steepness_deg
 
-_CHUNK = 2048  # the reference's work unit (simulate.py:39); kept as the shard block
 _FLAT_DIR_EPS = 1e-9
 _HALF_PI = math.pi / 2.0
 
@@ -102,14 +101,24 @@ class SnowParams:
 
 
 class ReleaseMask(Resident):
-    """Boolean raster marking particle release cells (simulate.py:135-156)."""
+    """Boolean raster marking particle release cells (simulate.py:135-156).
+
+    Masks produced by the steepness band (detect_release_points,
+    release_mask_from_dem) carry the producing kernel's device counters: the
+    set-cell count and ``borderline``, the lattice cells whose slope lies
+    within 1e-9 degrees of a band edge (the mask's guard band, SURVEY 8a
+    rows a7/a8).  Other device masks count through the compaction that
+    ``release_cells`` runs anyway (its cell list is kept on the mask)."""
 
     _payload = ("mask",)
     _dtypes = {"mask": (np.dtype(np.bool_), torch.bool)}
 
-    def __init__(self, mask):
+    def __init__(self, mask, *, _counts: torch.Tensor | None = None):
         super().__init__(mask=mask)
         object.__setattr__(self, "_count", None)
+        object.__setattr__(self, "_borderline", None)
+        object.__setattr__(self, "_counts_dev", _counts)
+        object.__setattr__(self, "_cells", None)
 
     @property
     def nrows(self) -> int:
@@ -119,14 +128,30 @@ class ReleaseMask(Resident):
     def ncols(self) -> int:
         return self.shape_of("mask")[1]
 
+    def _read_counts(self) -> None:
+        n, near = _device.read_small(self._counts_dev)
+        object.__setattr__(self, "_count", int(n))
+        object.__setattr__(self, "_borderline", int(near))
+        object.__setattr__(self, "_counts_dev", None)
+
     @property
     def count(self) -> int:
         if self._count is None:
-            if self.on_device("mask"):
-                object.__setattr__(self, "_count", int(_device.read_small(self.dev("mask").sum(dtype=torch.int64).reshape(1))[0]))
+            if self._counts_dev is not None:
+                self._read_counts()
+            elif self.on_device("mask"):
+                object.__setattr__(self, "_count", int(release_cells(self).numel()))
             else:
                 object.__setattr__(self, "_count", int(self._h["mask"].sum()))
         return self._count
+
+    @property
+    def borderline(self) -> int | None:
+        """Lattice cells within 1e-9 degrees of a band edge (None for masks
+        not produced from a slope band)."""
+        if self._counts_dev is not None:
+            self._read_counts()
+        return self._borderline
 
     def __repr__(self) -> str:
         return f"ReleaseMask({self.nrows}x{self.ncols})"
@@ -257,12 +282,13 @@ def detect_release_points(
     L = _lib.lib()
     s = slope.dev("slope_deg")
     out = _device.empty(tuple(s.shape), torch.uint8)
+    counts = _device.zeros((2,), torch.int64)
     _lib.check(
         L.wg_release_mask(_lib.ptr(s), slope.nrows, slope.ncols, float(min_steepness_deg), float(max_steepness_deg),
-                          int(stride), _lib.ptr(out), _lib.stream_ptr()),
+                          int(stride), _lib.ptr(out), _lib.ptr(counts), _lib.stream_ptr()),
         ParamError,
     )
-    return ReleaseMask(out.view(torch.bool))
+    return ReleaseMask(out.view(torch.bool), _counts=counts)
 
 
 def release_mask_from_dem(
@@ -286,14 +312,15 @@ def release_mask_from_dem(
     L = _lib.lib()
     e = grid.device_elevations()
     out = _device.empty((grid.nrows, grid.ncols), torch.uint8)
+    counts = _device.zeros((2,), torch.int64)
     cs = grid.cellsize
     _lib.check(
         L.wg_lattice_release_mask(_lib.ptr(e), grid.nrows, grid.ncols, cs, 2.0 * cs, float(min_steepness_deg),
                                   float(max_steepness_deg), int(stride), 0, grid.nrows, _lib.ptr(out),
-                                  _lib.stream_ptr()),
+                                  _lib.ptr(counts), _lib.stream_ptr()),
         ParamError,
     )
-    return ReleaseMask(out.view(torch.bool))
+    return ReleaseMask(out.view(torch.bool), _counts=counts)
 
 
 # -- the particle engine (csrc/traj.cu) ----------------------------------------
@@ -346,7 +373,10 @@ def _sc_args(sc: _Scalars) -> tuple:
 
 def release_cells(mask: ReleaseMask) -> torch.Tensor:
     """Row-major flat indices of the set mask cells (np.flatnonzero order,
-    simulate.py:465) by device stream compaction (wg_mask_compact)."""
+    simulate.py:465) by device stream compaction (wg_mask_compact); kept on
+    the (immutable) mask for later calls."""
+    if mask._cells is not None:
+        return mask._cells
     L = _lib.lib()
     m = mask.dev("mask").view(torch.uint8).reshape(-1)
     n = m.numel()
@@ -356,25 +386,24 @@ def release_cells(mask: ReleaseMask) -> torch.Tensor:
     _lib.check(L.wg_mask_compact(_lib.ptr(m), n, _lib.ptr(cells), _lib.ptr(count), _lib.ptr(scratch),
                                  _lib.stream_ptr()))
     k = int(_device.read_small(count.reshape(-1)[:1])[0])
-    return cells[:k]
+    object.__setattr__(mask, "_cells", cells[:k])
+    if mask._count is None:
+        object.__setattr__(mask, "_count", k)
+    return mask._cells
 
 
-def _world() -> tuple[int, int]:
-    import torch.distributed as dist
-
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        return dist.get_rank(), dist.get_world_size()
-    return 0, 1
+_LAYOUT_HEADROOM = 8 << 30  # HBM left free after a gather layout (NCCL, peers, the next rasters)
 
 
 def _try_empty(n: int) -> torch.Tensor | None:
-    """A transient float64 buffer, or None when HBM cannot hold it (the
-    allocation attempt is the fit test: cheaper than querying the driver's
-    free memory on every launch, and the buffer is released to the caching
-    allocator as soon as the trajectory launch is queued)."""
+    """A float64 buffer of n elements, or None when it would leave less than
+    _LAYOUT_HEADROOM of HBM free: the driver's free memory (other processes,
+    the context, NCCL) plus what the caching allocator holds unused."""
     dev = _device.device()
-    if 8 * n > torch.cuda.get_device_properties(dev).total_memory - torch.cuda.memory_allocated(dev):
-        return None  # cannot fit: skip the attempt (a failed one flushes the allocator's cache)
+    free, _ = torch.cuda.mem_get_info(dev)
+    spare = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    if 8 * n + _LAYOUT_HEADROOM > free + spare:
+        return None
     try:
         return _device.empty((n,), torch.float64)
     except torch.cuda.OutOfMemoryError:
@@ -416,6 +445,24 @@ def build_gather_layout(grid: DemGrid) -> tuple[torch.Tensor | None, torch.Tenso
     return None, build_pair(grid)
 
 
+def gather_layout(grid: DemGrid) -> tuple[torch.Tensor | None, torch.Tensor | None, torch.Tensor]:
+    """(quad, pair, absmax) of an immutable grid, built on first use and kept
+    on the grid: the trajectory kernel's gather layout and the bits of max
+    |z| (the operand bound of its divisions) -- one 1.6 ms / 10.7 GB pass at
+    16384^2 per grid instead of per launch."""
+    cached = grid._gather
+    if cached is not None:
+        return cached
+    L = _lib.lib()
+    e = grid.device_elevations()
+    absmax = _device.empty((1,), torch.int64)
+    _lib.check(L.wg_absmax(_lib.ptr(e), e.numel(), _lib.ptr(absmax), _lib.stream_ptr()), ParamError)
+    quad, pair = build_gather_layout(grid)
+    cached = (quad, pair, absmax)
+    object.__setattr__(grid, "_gather", cached)
+    return cached
+
+
 def run_avalanche_device(
     grid: DemGrid,
     cells: torch.Tensor,
@@ -423,33 +470,40 @@ def run_avalanche_device(
     *,
     i_lo: int = 0,
     i_hi: int | None = None,
-    rank: int = 0,
-    nranks: int = 1,
-    shard_block: int = _CHUNK,
+    ranges: list[tuple[int, int]] | None = None,
     hits: torch.Tensor | None = None,
     zmax: torch.Tensor | None = None,
+    touched: torch.Tensor | None = None,
+    tile_log2: int = 6,
     stream: torch.cuda.Stream | None = None,
 ) -> tuple[torch.Tensor, torch.Tensor]:
-    """Launch the trajectory kernel over particles [i_lo, i_hi) (this rank's
-    blocked-cyclic share) accumulating into (hits, zmax); no host sync."""
+    """Launch the trajectory kernel over the particles [i_lo, i_hi) (or the
+    ascending disjoint `ranges`, a rank's bands) accumulating into (hits,
+    zmax) and, when given, the touched-tile map; no host sync."""
     L = _lib.lib()
     sc = kernel_scalars(grid, params)
     total = int(cells.numel()) * params.particles_per_release_cell
-    if i_hi is None:
-        i_hi = total
+    if ranges is None:
+        ranges = [(int(i_lo), total if i_hi is None else int(i_hi))]
+    ranges = [(int(a), int(b)) for a, b in ranges]
     if hits is None:
         hits = _device.zeros((grid.nrows, grid.ncols), torch.int64)
     if zmax is None:
         zmax = _device.zeros((grid.nrows, grid.ncols), torch.float64)
-    scratch = _device.empty((int(L.wg_avalanche_scratch_bytes(params.particles_per_release_cell, int(i_lo),
-                                                               int(i_hi))),), torch.uint8)
+    if all(b <= a for a, b in ranges):
+        return hits, zmax
+    span_lo, span_hi = ranges[0][0], ranges[-1][1]
+    scratch = _device.empty((int(L.wg_avalanche_scratch_bytes(params.particles_per_release_cell, span_lo,
+                                                               span_hi)),), torch.uint8)
     dem = grid.device_elevations()
-    quad, pair = build_gather_layout(grid) if int(i_hi) > int(i_lo) else (None, None)
+    quad, pair, absmax = gather_layout(grid)
+    pairs = (ctypes.c_int64 * (2 * len(ranges)))(*[v for r in ranges for v in r])
     _lib.check(
         L.wg_run_avalanche(
-            _lib.ptr(dem), _lib.ptr(quad), _lib.ptr(pair), *_sc_args(sc), _lib.ptr(cells), params.particles_per_release_cell,
-            rng.seed_word(params.seed), int(i_lo), int(i_hi), int(shard_block), int(rank), int(nranks),
-            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(scratch), _lib.stream_ptr(stream),
+            _lib.ptr(dem), _lib.ptr(quad), _lib.ptr(pair), *_sc_args(sc), _lib.ptr(cells),
+            params.particles_per_release_cell, rng.seed_word(params.seed), pairs, len(ranges), _lib.ptr(absmax),
+            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(touched), int(tile_log2), _lib.ptr(scratch),
+            _lib.stream_ptr(stream),
         ),
         ParamError,
     )
@@ -461,10 +515,15 @@ def run_avalanche(
     mask: ReleaseMask,
     params: AvalancheParams,
     threads: int = 1,
+    *,
+    group=None,
 ) -> RunoutRaster:
     """Release particles from every marked cell and accumulate the flow
     (simulate.py:441-504).  ``threads`` is validated like the reference and
-    otherwise ignored: the GPU result is bitwise independent of any schedule."""
+    otherwise ignored: the GPU result is bitwise independent of any schedule.
+    ``group`` (a torch.distributed process group, one GPU per rank, every
+    rank calling with the same grid and mask) shards the particles over its
+    ranks; each rank returns the whole raster."""
     if (mask.nrows, mask.ncols) != (grid.nrows, grid.ncols):
         raise SimulationError(
             f"mask shape {(mask.nrows, mask.ncols)} does not match grid {(grid.nrows, grid.ncols)}"
@@ -474,16 +533,17 @@ def run_avalanche(
     if grid.has_nodata():
         raise SimulationError("simulation requires a gap-free grid")
     cells = release_cells(mask)
+    if group is not None:
+        from . import shard
+
+        run = shard.run_sharded(grid, cells, params, group)
+        shard.gather_bands(run.hits, run.zmax, run.plan, group)
+        return RunoutRaster(run.zmax, run.hits, _deferred=True)
     hits = _device.zeros((grid.nrows, grid.ncols), torch.int64)
     zmax = _device.zeros((grid.nrows, grid.ncols), torch.float64)
     if cells.numel() == 0:
         return RunoutRaster(zmax, hits, _deferred=True)
-    rank, world = _world()
-    run_avalanche_device(grid, cells, params, rank=rank, nranks=world, hits=hits, zmax=zmax)
-    if world > 1:
-        from .shard import merge_runout
-
-        merge_runout(hits, zmax)
+    run_avalanche_device(grid, cells, params, hits=hits, zmax=zmax)
     return RunoutRaster(zmax, hits, _deferred=True)
 
 

@@ -72,5 +72,7 @@ def synth_grid(n: int, seed: int, cs: float = 10.0, device: bool = True):
     """DemGrid over synth_dem (origin (0, 0), nodata -9999)."""
     from .grid import DemGrid
 
-    elev = synth_dem_device(n, seed, cs) if device else synth_dem_host(n, seed, cs)
-    return DemGrid(ncols=n, nrows=n, origin_x=0.0, origin_y=0.0, cellsize=cs, nodata=-9999.0, elevations=elev)
+    if device:
+        return DemGrid.adopt(n, n, 0.0, 0.0, cs, -9999.0, synth_dem_device(n, seed, cs))
+    return DemGrid(ncols=n, nrows=n, origin_x=0.0, origin_y=0.0, cellsize=cs, nodata=-9999.0,
+                   elevations=synth_dem_host(n, seed, cs))

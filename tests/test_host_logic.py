@@ -183,14 +183,21 @@ def test_compute_nodes_fail_loudly_without_gpu():
     assert isinstance(ei.value.cause, NativeUnavailable)
 
 
-def test_shard_partition_covers_every_particle_once():
-    from paper_2506_23364_b200.shard import local_indices, local_particles
+def test_exchange_segments_group_foreign_tiles_by_owner():
+    from paper_2506_23364_b200 import shard
 
-    for total, block in ((0, 8), (1, 8), (8191, 2048), (10_000, 256), (12_288, 2048)):
-        for n in (1, 2, 3, 8):
-            seen = np.zeros(total, dtype=np.int32)
-            for r in range(n):
-                idx = [i for rg in local_indices(total, block, r, n) for i in rg]
-                assert len(idx) == local_particles(total, block, r, n)
-                seen[idx] += 1
-            assert (seen == 1).all()
+    plan = shard.plan_bands(1024, 1024, 4, 2, 6)  # 8 bands of 128 rows = 2 tile rows
+    rng = np.random.default_rng(1)
+    ids = np.unique(rng.integers(0, plan.tiles_x * plan.tiles_y, 100))
+    toffs = [int(v) for v in np.searchsorted(ids, plan.tile_bounds())]
+    for rank in range(4):
+        segs, counts = shard.exchange_segments(toffs, plan, rank)
+        assert counts[rank] == 0
+        out = np.concatenate([ids[s:s + n] for s, _, n in segs])
+        # every foreign tile exactly once, grouped by destination rank in rank order
+        owners = [plan.owner(int(t) // plan.tiles_x * plan.tile // plan.band_rows) for t in out]
+        assert owners == sorted(owners) and rank not in owners
+        foreign = [t for t in ids if plan.owner(int(t) // plan.tiles_x * plan.tile // plan.band_rows) != rank]
+        assert sorted(out.tolist()) == sorted(int(t) for t in foreign)
+        assert sum(counts) == len(out)
+        assert [s[1] for s in segs] == list(np.cumsum([0] + [s[2] for s in segs])[:-1])

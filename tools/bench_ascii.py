@@ -36,7 +36,7 @@ def main():
     _lib.build()
     L = _lib.lib()
     n = a.size
-    g = wf.DemGrid(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 0))
+    g = wf.DemGrid.adopt(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 0))
     count = n * n
 
     # ---- writer: kernels only (values resident, text stays on the device)

@@ -98,7 +98,7 @@ def main():
     _lib.build()
     L = _lib.lib()
     n = 8192
-    dem = wf.DemGrid(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
+    dem = wf.DemGrid.adopt(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
     hs = hillshade_pyramid(dem)
     g = wf.build_avalanche_graph(dem.extent, wf.AvalancheParams(particles_per_release_cell=256, seed=0),
                                  wf.SteepnessRelease(30.0, 45.0, stride=16), zoom=2)

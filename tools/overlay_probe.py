@@ -15,7 +15,7 @@ from paper_2506_23364_b200.synth import synth_dem_device  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 stride = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 ppc = int(sys.argv[3]) if len(sys.argv) > 3 else 256
-world = wf.DemGrid(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
+world = wf.DemGrid.adopt(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
 for rep in range(int(sys.argv[4]) if len(sys.argv) > 4 else 3):
     g = wf.build_avalanche_graph(world.extent, wf.AvalancheParams(particles_per_release_cell=ppc, seed=rep),
                                  wf.SteepnessRelease(30.0, 45.0, stride=stride), zoom=2)

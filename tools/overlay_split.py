@@ -39,7 +39,7 @@ for mod, name in ((simulate, "_try_empty"), (_device, "empty"), (simulate, "buil
     if hasattr(mod, name):
         wrap(mod, name)
 
-world = wf.DemGrid(8192, 8192, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(8192, 1))
+world = wf.DemGrid.adopt(8192, 8192, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(8192, 1))
 for rep in range(3):
     marks.clear()
     g = wf.build_avalanche_graph(world.extent, wf.AvalancheParams(particles_per_release_cell=256, seed=rep),

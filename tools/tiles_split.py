@@ -14,7 +14,7 @@ from paper_2506_23364_b200 import _device, _lib, overlay  # noqa: E402
 from paper_2506_23364_b200.synth import synth_dem_device  # noqa: E402
 
 n = 8192
-dem = wf.DemGrid(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
+dem = wf.DemGrid.adopt(n, n, 0.0, 0.0, 10.0, -9999.0, synth_dem_device(n, 1))
 g = wf.build_avalanche_graph(dem.extent, wf.AvalancheParams(particles_per_release_cell=256, seed=0),
                              wf.SteepnessRelease(30.0, 45.0, stride=16), zoom=2)
 g.bind("world", dem)
