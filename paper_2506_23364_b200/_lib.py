@@ -64,7 +64,7 @@ SIGNATURES: dict[str, tuple] = {
     "wg_trace_particle": (
         c_int,
         [c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_i64,
-         c_dbl, c_dbl, c_u64, c_ptr, c_i64, c_ptr, c_ptr],
+         c_dbl, c_dbl, c_dbl, c_u64, c_ptr, c_i64, c_ptr, c_ptr],
     ),
     "wg_particle_records": (
         c_int,

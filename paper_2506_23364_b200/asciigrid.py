@@ -159,11 +159,15 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
     L = _lib.lib()
     dev = _device.device()
     n = len(data)
+    # a body of m bytes holds at most (m + 1) // 2 tokens: a header that
+    # promises more cannot be satisfied, and must not size the allocations
+    # (the reader then only counts, and the reference's message follows)
+    cap = min(expected, (n - body_off + 1) // 2)
     t = _device.upload(np.frombuffer(data, dtype=np.uint8))
-    values = torch.empty(expected, dtype=torch.float64, device=dev)
+    values = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
     info = torch.empty(4, dtype=torch.int64, device=dev)
-    scratch = torch.empty(int(L.wg_ascii_read_scratch_bytes(n, expected)), dtype=torch.uint8, device=dev)
-    _lib.check(L.wg_ascii_read(_lib.ptr(t), n, body_off, _lib.ptr(values), expected, _lib.ptr(info),
+    scratch = torch.empty(int(L.wg_ascii_read_scratch_bytes(n, cap)), dtype=torch.uint8, device=dev)
+    _lib.check(L.wg_ascii_read(_lib.ptr(t), n, body_off, _lib.ptr(values), cap, _lib.ptr(info),
                                _lib.ptr(scratch), _lib.stream_ptr()), AsciiGridError)
     found, nonascii, extra_off, bad_off = (v & _NO_BAD for v in _device.read_small(info))
     if nonascii:

@@ -30,6 +30,7 @@ from .overlay import OverlayTexture
 from .terrain import NormalField, SlopeField, steepness_deg
 
 _FLAT_DIR_EPS = 1e-9
+FLAT_GRADIENT_THRESHOLD = 1e-6  # terrain.py:19 (re-exported by the reference's simulate)
 _HALF_PI = math.pi / 2.0
 
 
@@ -560,18 +561,25 @@ def simulate_particle(
     if not grid.contains(start[0], start[1]):
         raise SimulationError(f"start {start} outside grid extent")
     key = stream.key if stream is not None else rng.derive_key(params.seed, 0, 0)
+    positions, code = trace(grid, start, params, key, grid.cellsize)
+    return Trajectory(positions=positions, stop_reason=_REASON_BY_CODE[code])
+
+
+def trace(grid: DemGrid, start: tuple[float, float], params: AvalancheParams, key: int,
+          step: float) -> tuple[np.ndarray, int]:
+    """One particle's path on the device (wg_trace_particle): (positions, stop code)."""
     L = _lib.lib()
     sc = kernel_scalars(grid, params)
     cap = int(sc.max_steps) + 2
     path = _device.empty((cap, 2), torch.float64)
     meta = _device.zeros((2,), torch.int64)
     _lib.check(
-        L.wg_trace_particle(_lib.ptr(grid.device_elevations()), *_sc_args(sc), float(start[0]), float(start[1]),
-                            int(key), _lib.ptr(path), cap, _lib.ptr(meta), _lib.stream_ptr()),
+        L.wg_trace_particle(_lib.ptr(grid.device_elevations()), *_sc_args(sc), float(step), float(start[0]),
+                            float(start[1]), int(key), _lib.ptr(path), cap, _lib.ptr(meta), _lib.stream_ptr()),
         ParamError,
     )
     n, code = meta.tolist()
-    return Trajectory(positions=path[:n].cpu().numpy(), stop_reason=_REASON_BY_CODE[code])
+    return path[:n].cpu().numpy(), code
 
 
 def particle_records(

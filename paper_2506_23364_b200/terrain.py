@@ -1,8 +1,9 @@
 """Surface derivatives of elevation grids (mirrors demflow/terrain.py).
 
 compute_normals / steepness_deg / hillshade run as sm_100a kernels
-(csrc/stencil.cu); downslope_dir is a scalar query helper evaluated on the
-host with the reference's arithmetic (terrain.py:105-148).
+(csrc/stencil.cu); oracle_descent_path runs the trajectory kernel's step
+function (csrc/traj.cu) on one lane; downslope_dir is a scalar query helper
+evaluated on the host with the reference's arithmetic (terrain.py:105-148).
 """
 
 from __future__ import annotations
@@ -158,6 +159,37 @@ def downslope_dir(grid: DemGrid, x: float, y: float) -> tuple[float, float] | No
     if mag < FLAT_GRADIENT_THRESHOLD:
         return None
     return (gx / mag, gy / mag)
+
+
+def oracle_descent_path(
+    grid: DemGrid,
+    start: tuple[float, float],
+    step: float,
+    runout_angle_deg: float = 25.0,
+    max_steps: int | None = None,
+) -> tuple[np.ndarray, str]:
+    """Steepest-descent walk from `start` in `step`-metre steps (terrain.py:151-284):
+    stops on flat ground, on leaving the grid (exit point clipped to the
+    border and kept), when the angle back up to the start drops below
+    `runout_angle_deg`, or after the step cap (10 * max(ncols, nrows) by
+    default).  Returns (positions (n, 2), reason).
+
+    The reference keeps this walk free of the particle engine's code while
+    matching its float sequence for a memoryless, jitter-free particle; here
+    it is exactly that particle -- persistence 0 (the blend reduces to the
+    renormalised descent direction bit for bit), randomness 0 -- traced by
+    the device step function with the step length set to `step`."""
+    from .simulate import AvalancheParams, trace
+
+    if grid.has_nodata():
+        raise SampleError("descent path on a grid with nodata")
+    x, y = float(start[0]), float(start[1])
+    if not grid.contains(x, y):
+        raise SampleError(f"start ({x}, {y}) outside grid extent")
+    params = AvalancheParams(persistence=0.0, randomness=0.0, runout_angle_deg=runout_angle_deg,
+                             max_steps=max_steps)
+    positions, code = trace(grid, (x, y), params, 0, float(step))
+    return positions, ("RUNOUT_ANGLE", "DOMAIN_EXIT", "FLAT", "MAX_STEPS")[code]
 
 
 def _light(azimuth_deg: float, altitude_deg: float) -> tuple[float, float, float]:

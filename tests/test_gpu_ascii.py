@@ -62,6 +62,18 @@ def test_parse_accepts_bytes(ag):
     assert np.array_equal(np.asarray(a.elevations), np.asarray(b.elevations))
 
 
+def test_huge_header_small_body(ag):
+    """A header promising 10^12 values over a tiny body raises the
+    reference's count error (its messages, run here: 'found 3 (line 7)',
+    'found 0 (line 6)') without sizing any buffer by the header."""
+    head = "ncols 1000000\nnrows 1000000\nxllcorner 0\nyllcorner 0\ncellsize 1\nNODATA_value -9999\n"
+    for body, msg in (("1 2 3\n", "expected 1000000000000 elevation values, found 3 (line 7)"),
+                      ("", "expected 1000000000000 elevation values, found 0 (line 6)")):
+        with pytest.raises(ag.AsciiGridError) as ei:
+            ag.parse_ascii_grid(head + body)
+        assert str(ei.value) == msg
+
+
 def test_non_ascii_document_rejected(ag):
     with pytest.raises(ag.AsciiGridError):
         ag.parse_ascii_grid(GOLDEN["parse"][0]["doc"].replace("1 2", "1 2"))

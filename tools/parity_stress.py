@@ -1,42 +1,17 @@
-"""Randomised parity stress of the trajectory kernel vs the C oracle (60 seeded worlds:
-shapes 20-300, cellsizes 0.5-100, origins up to 1e6, terraced terrain every 7th case,
-random release sets and parameters).  usage: python tools/parity_stress.py"""
+"""Randomised parity stress of the trajectory kernel vs the C oracle: the 60
+seeded worlds of tests/test_gpu_stress.py, run as a script (exit status 1 on
+any mismatch).  usage: python tools/parity_stress.py"""
 import sys
 from pathlib import Path
 
-import numpy as np
-
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
 import paper_2506_23364_b200 as wf  # noqa: E402
-from oracle import traj  # noqa: E402
-from paper_2506_23364_b200.synth import synth_dem_host  # noqa: E402
+from test_gpu_stress import CASES, run_case  # noqa: E402
 
-
-def bits(a):
-    return np.ascontiguousarray(a).view(np.int64)
-
-
-
-bad = 0
-for case in range(100, 160):
-    r = np.random.default_rng(1000 + case)
-    nr, nc = int(r.integers(20, 300)), int(r.integers(20, 300))
-    cs = float(r.choice([0.5, 3.7, 10.0, 25.0, 1.0 / 3.0, 100.0]))
-    ox, oy = float(r.uniform(-1e6, 1e6)), float(r.uniform(-1e6, 1e6))
-    e = synth_dem_host(max(nr, nc), int(case) % 50)[:nr, :nc] * float(r.uniform(0.01, 5.0)) * (cs / 10.0)
-    e = e + r.uniform(-80, 80) * np.linspace(0, 1, nc)[None, :] + r.uniform(-80, 80) * np.linspace(0, 1, nr)[:, None]
-    if case % 7 == 0:
-        e = np.round(e, 1)  # terraces / plateaus
-    e = np.ascontiguousarray(e)
-    mask = r.random((nr, nc)) < float(r.uniform(0.002, 0.05))
-    params = {"particles_per_release_cell": int(r.integers(1, 64)), "seed": int(r.integers(0, 2**63)),
-              "persistence": float(r.uniform(0, 1)), "randomness": float(r.uniform(0, 1)),
-              "runout_angle_deg": float(r.uniform(1, 60))}
-    grid = wf.DemGrid(ncols=nc, nrows=nr, origin_x=ox, origin_y=oy, cellsize=cs, nodata=-9999.0, elevations=e)
-    run = wf.run_avalanche(grid, wf.ReleaseMask(mask), wf.AvalancheParams(**params))
-    z, h = traj.run_avalanche(e, ox, oy, cs, mask, **params)
-    ok = np.array_equal(run.hit_count, h) and np.array_equal(bits(run.z_delta_max), bits(z))
-    if not ok:
-        bad += 1
-        print("MISMATCH", case, nr, nc, cs, params)
-print("cases", 60, "bad", bad)
+bad = [case for case in CASES if not run_case(wf, case)]
+for case in bad:
+    print("MISMATCH", case)
+print("cases", len(CASES), "bad", len(bad))
+sys.exit(1 if bad else 0)
