@@ -16,14 +16,20 @@ formatted by csrc/asciigrid.cu:
 
 Errors are the reference's ``AsciiGridError`` messages with the same 1-based
 line / column positions (computed on the host, on the error path only).
-Documents must be ASCII (the ESRI format is); other text raises
-``AsciiGridError`` instead of being split on Unicode whitespace.
+A ``str`` document with non-ASCII characters is first translated one
+character for one (``_asciify``), the way CPython's own float() reads text:
+Unicode whitespace becomes a space (non-ASCII line boundaries a newline, so
+``splitlines`` numbering is kept), Unicode decimal digits their ASCII digit,
+anything else a character float() rejects -- so the tokens, values, line /
+column positions and rejected tokens are the reference's (``str.split`` /
+``float``); byte input must be ASCII.
 """
 
 from __future__ import annotations
 
 import math
 import re
+import unicodedata
 
 import numpy as np
 import torch
@@ -64,13 +70,39 @@ def format_number(v: float) -> str:
     return repr(f)
 
 
+# str.splitlines() boundaries outside ASCII
+_UNICODE_LINE_BREAKS = frozenset("\x85\u2028\u2029")
+
+
+def _asciify(text: str) -> bytes:
+    """One ASCII byte per character of `text`, with the structure str.split /
+    str.splitlines / float() see in it: non-ASCII line boundaries -> '\\n',
+    other Unicode whitespace -> ' ', Unicode decimal digits -> their ASCII
+    digit (float() converts them: CPython's _PyUnicode_TransformDecimalAndSpaceToASCII),
+    any other non-ASCII character -> '?' (which float() rejects, as it
+    rejects the character).  Offsets are preserved, so positions and
+    offending tokens map back to the original text."""
+    table = {}
+    for ch in set(text):
+        if ch.isascii():
+            continue
+        if ch in _UNICODE_LINE_BREAKS:
+            table[ord(ch)] = "\n"
+        elif ch.isspace():
+            table[ord(ch)] = " "
+        else:
+            d = unicodedata.decimal(ch, None)
+            table[ord(ch)] = str(d) if d is not None else "?"
+    return text.translate(table).encode("ascii")
+
+
 def _as_bytes(text):
     if isinstance(text, (bytes, bytearray)):
         return text
     if isinstance(text, memoryview):
         return text if text.contiguous and text.format in ("B", "b", "c") else text.tobytes()
     if not text.isascii():
-        raise AsciiGridError("document is not ASCII")
+        return _asciify(text)
     return text.encode("ascii")
 
 
@@ -141,6 +173,7 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
     """Parse an ASCII grid document into a device-resident DemGrid
     (asciigrid.py:42-143)."""
     data = _as_bytes(text)
+    original = text if isinstance(text, str) and not text.isascii() else None  # for offending tokens
     if isinstance(data, memoryview):
         head = bytes(data[: 1 << 16])
         try:
@@ -185,7 +218,8 @@ def parse_ascii_grid(text: str | bytes) -> DemGrid:
                                                        b"\x1e", b"\x1f"):
             end += 1
         line, col = _line_col(data, bad_off)
-        raise AsciiGridError(f"invalid elevation value {data[bad_off:end].decode('ascii')!r}", line=line, column=col)
+        token = original[bad_off:end] if original is not None else data[bad_off:end].decode("ascii")
+        raise AsciiGridError(f"invalid elevation value {token!r}", line=line, column=col)
     del t, scratch
     try:
         return DemGrid.adopt(ncols, nrows, header["xllcorner"], header["yllcorner"], header["cellsize"],

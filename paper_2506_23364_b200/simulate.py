@@ -398,13 +398,18 @@ _LAYOUT_HEADROOM = 8 << 30  # HBM left free after a gather layout (NCCL, peers, 
 
 def _try_empty(n: int) -> torch.Tensor | None:
     """A float64 buffer of n elements, or None when it would leave less than
-    _LAYOUT_HEADROOM of HBM free: the driver's free memory (other processes,
-    the context, NCCL) plus what the caching allocator holds unused."""
+    _LAYOUT_HEADROOM of HBM free.  When this process's own allocations leave
+    ample room the buffer is taken directly; near the limit the driver's
+    free memory (other processes, the context, NCCL) plus what the caching
+    allocator holds unused decides -- cudaMemGetInfo is kept off the common
+    path, where it would cost a driver round trip per grid."""
     dev = _device.device()
-    free, _ = torch.cuda.mem_get_info(dev)
-    spare = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
-    if 8 * n + _LAYOUT_HEADROOM > free + spare:
-        return None
+    need = 8 * n + _LAYOUT_HEADROOM
+    if torch.cuda.get_device_properties(dev).total_memory - torch.cuda.memory_allocated(dev) < 4 * need:
+        free, _ = torch.cuda.mem_get_info(dev)
+        spare = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+        if need > free + spare:
+            return None
     try:
         return _device.empty((n,), torch.float64)
     except torch.cuda.OutOfMemoryError:

@@ -74,9 +74,25 @@ def test_huge_header_small_body(ag):
         assert str(ei.value) == msg
 
 
-def test_non_ascii_document_rejected(ag):
-    with pytest.raises(ag.AsciiGridError):
-        ag.parse_ascii_grid(GOLDEN["parse"][0]["doc"].replace("1 2", "1 2"))
+UNICODE = json.loads((Path(__file__).resolve().parent / "golden" / "ascii_unicode_golden.json").read_text())
+
+
+@pytest.mark.parametrize("case", UNICODE, ids=[c["name"] for c in UNICODE])
+def test_non_ascii_documents_like_reference(ag, case):
+    """Unicode separators / digits parse as the reference's str.split and
+    float() read them; other characters give its messages and positions
+    (tests/golden/make_ascii_unicode_golden.py ran the reference)."""
+    if "ok" in case:
+        g = ag.parse_ascii_grid(case["doc"])
+        assert (g.ncols, g.nrows) == (case["ok"]["ncols"], case["ok"]["nrows"])
+        assert np.asarray(g.elevations).ravel().tolist() == case["ok"]["values"]
+    else:
+        with pytest.raises(ag.AsciiGridError) as ei:
+            ag.parse_ascii_grid(case["doc"])
+        assert str(ei.value) == case["error"]
+
+
+def test_non_ascii_bytes_rejected(ag):
     with pytest.raises(ag.AsciiGridError):
         ag.parse_ascii_grid(GOLDEN["parse"][0]["doc"].encode().replace(b"1 2", b"1\xc2\xa02"))
 
