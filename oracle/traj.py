@@ -91,7 +91,8 @@ def run_range(elev, ox, oy, cs, cells, lo, hi, hits, zmax, *, persistence=0.9, r
               runout_angle_deg=25.0, particles_per_release_cell=2048, seed=0, max_steps=None, threads=None,
               records=False):
     """Particles [lo, hi) accumulated into caller-owned rasters (one shared
-    pair across calls, unlike the reference's per-chunk partials); returns
+    pair across calls, unlike the reference's per-chunk partials; None for
+    records-only runs); returns
     the particle steps taken, and with records=True also the per-particle
     (reason, steps, end) arrays."""
     n = hi - lo
@@ -102,7 +103,8 @@ def run_range(elev, ox, oy, cs, cells, lo, hi, hits, zmax, *, persistence=0.9, r
     ends = np.zeros((n, 2), dtype=np.float64) if records else None
     lib().orc_run_particles(
         *world_args(elev, ox, oy, cs, persistence, randomness, runout_angle_deg, max_steps),
-        cells.ctypes.data, particles_per_release_cell, seed & MASK64, lo, hi, hits.ctypes.data, zmax.ctypes.data,
+        cells.ctypes.data, particles_per_release_cell, seed & MASK64, lo, hi,
+        hits.ctypes.data if hits is not None else None, zmax.ctypes.data if zmax is not None else None,
         reasons.ctypes.data if records else None, steps.ctypes.data, ends.ctypes.data if records else None,
         int(threads or os.cpu_count() or 1),
     )

@@ -86,13 +86,18 @@ __device__ __forceinline__ void add_counts(unsigned long long* counts, unsigned 
 // five divisions through shared reciprocals with one guard for all of them
 // -- the rare guard miss recomputes the cell with __ddiv_rn.  Shared by the
 // normals pass and the lattice mask so both give the same bits.
+// kInterior: the caller knows the cell is not on a border (a warp-uniform
+// test in the normals pass), so the border selects drop out.
+template <bool kInterior = false>
 __device__ __forceinline__ void cell_normal(double cur, double west, double east, double up, double dn, int i, int jc,
                                             int nrows, int ncols, double cs, double two_cs, double rcs, double r2cs,
                                             bool cs_ok, double& n0, double& n1, double& nz) {
-  const bool xb = (jc == 0) | (jc == ncols - 1), yb = (i == 0) | (i == nrows - 1);
-  const double xa = WG_SUB(jc == 0 ? east : (jc == ncols - 1 ? cur : east),
-                           jc == 0 ? cur : (jc == ncols - 1 ? west : west));
-  const double ya = WG_SUB(i == 0 ? cur : up, i == 0 ? dn : (i == nrows - 1 ? cur : dn));
+  const bool xb = !kInterior && ((jc == 0) | (jc == ncols - 1));
+  const bool yb = !kInterior && ((i == 0) | (i == nrows - 1));
+  const double xa = kInterior ? WG_SUB(east, west)
+                              : WG_SUB(jc == 0 ? east : (jc == ncols - 1 ? cur : east),
+                                       jc == 0 ? cur : (jc == ncols - 1 ? west : west));
+  const double ya = kInterior ? WG_SUB(up, dn) : WG_SUB(i == 0 ? cur : up, i == 0 ? dn : (i == nrows - 1 ? cur : dn));
   const double xd = xb ? cs : two_cs, xr = xb ? rcs : r2cs;
   const double yd = yb ? cs : two_cs, yr = yb ? rcs : r2cs;
   bool ok = cs_ok;
@@ -144,6 +149,7 @@ __global__ void __launch_bounds__(kNormThreads, WG_NORM_MINB) normals_kernel(con
   const double rcs = rcp_refined(cs), r2cs = rcp_refined(two_cs);
   const bool cs_fast = b_ok(cs), c2_fast = b_ok(two_cs);
   const double* col = e + jc;
+  const bool interior_cols = jw0 > 0 && jw0 + 32 < ncols;  // no lane of the warp on the west / east border
   double up = i0 > 0 ? __ldg(col + (size_t)(i0 - 1) * ncols) : 0.0;
   double cur = __ldg(col + (size_t)i0 * ncols);
   // the row below is loaded one iteration ahead, so its latency overlaps a
@@ -158,7 +164,10 @@ __global__ void __launch_bounds__(kNormThreads, WG_NORM_MINB) normals_kernel(con
     if (lane == 0 && jc > 0) west = __ldg(row + jc - 1);
     if ((lane == 31 || j + 1 >= ncols) && jc + 1 < ncols) east = __ldg(row + jc + 1);
     double n0, n1, nz;
-    cell_normal(cur, west, east, up, dn, i, jc, nrows, ncols, cs, two_cs, rcs, r2cs, cs_fast && c2_fast, n0, n1, nz);
+    if (interior_cols && i > 0 && i < nrows - 1)  // warp-uniform
+      cell_normal<true>(cur, west, east, up, dn, i, jc, nrows, ncols, cs, two_cs, rcs, r2cs, c2_fast, n0, n1, nz);
+    else
+      cell_normal(cur, west, east, up, dn, i, jc, nrows, ncols, cs, two_cs, rcs, r2cs, cs_fast && c2_fast, n0, n1, nz);
     const size_t cell = (size_t)i * ncols + j;
     if (slope != nullptr && live) slope[cell] = slope_of(nz);
     if (nrm != nullptr) {

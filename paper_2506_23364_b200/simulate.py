@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import weakref
 from dataclasses import dataclass, replace
 from enum import Enum
 
@@ -451,11 +452,17 @@ def build_gather_layout(grid: DemGrid) -> tuple[torch.Tensor | None, torch.Tenso
     return None, build_pair(grid)
 
 
+_LAYOUT_GRIDS = 2  # grids that keep their gather layout (4x / 2x the DEM each)
+_layout_owners: list = []  # weak references to them, oldest first
+
+
 def gather_layout(grid: DemGrid) -> tuple[torch.Tensor | None, torch.Tensor | None, torch.Tensor]:
     """(quad, pair, absmax) of an immutable grid, built on first use and kept
     on the grid: the trajectory kernel's gather layout and the bits of max
     |z| (the operand bound of its divisions) -- one 1.6 ms / 10.7 GB pass at
-    16384^2 per grid instead of per launch."""
+    16384^2 per grid instead of per launch.  Only the _LAYOUT_GRIDS most
+    recent grids keep theirs (an executor's cache may hold many grids; a
+    layout is four times the DEM)."""
     cached = grid._gather
     if cached is not None:
         return cached
@@ -463,9 +470,15 @@ def gather_layout(grid: DemGrid) -> tuple[torch.Tensor | None, torch.Tensor | No
     e = grid.device_elevations()
     absmax = _device.empty((1,), torch.int64)
     _lib.check(L.wg_absmax(_lib.ptr(e), e.numel(), _lib.ptr(absmax), _lib.stream_ptr()), ParamError)
+    _layout_owners[:] = [r for r in _layout_owners if r() is not None]
+    while len(_layout_owners) >= _LAYOUT_GRIDS:
+        old = _layout_owners.pop(0)()
+        if old is not None:
+            object.__setattr__(old, "_gather", None)  # freed once its launches are done (stream-ordered)
     quad, pair = build_gather_layout(grid)
     cached = (quad, pair, absmax)
     object.__setattr__(grid, "_gather", cached)
+    _layout_owners.append(weakref.ref(grid))
     return cached
 
 
