@@ -291,15 +291,15 @@ def main() -> None:
         offs = shard.band_cell_offsets(cells, plan)
         ranges = shard.particle_ranges(offs, plan, rank, a.ppc)
         e0.record(stream)
-        run_avalanche_device(g, cells, params, ranges=ranges, hits=hits, zmax=zmax, touched=touched,
-                             tile_log2=plan.tile_log2)
+        run_avalanche_device(g, cells, params, ranges=ranges, hits=hits, zmax=zmax, touched=touched, plan=plan,
+                             rank=rank)
         e1.record(stream)
         m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         m0.record(stream)
         traffic = shard.merge_tiles(hits, zmax, touched, plan)
         m1.record(stream)
         total_hits, _, _ = shard.band_stats(hits, zmax, plan)  # invariants + stats of the owned bands
-        shard.clear_tiles(hits, zmax, touched, plan)
+        shard.clear_tiles(hits, zmax, touched, plan, rank)
         return total_hits, cells, (e0, e1), (m0, m1), dict(traffic, ranges=len(ranges),
                                                            local_particles=shard.local_particles(ranges))
 

@@ -52,7 +52,8 @@ SIGNATURES: dict[str, tuple] = {
     "wg_run_avalanche": (
         c_int,
         [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl,
-         c_i64, c_ptr, c_i64, c_u64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_int, c_ptr, c_ptr],
+         c_i64, c_ptr, c_i64, c_u64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_int, c_int, c_int, c_int, c_ptr,
+         c_ptr],
     ),
     "wg_absmax": (c_int, [c_ptr, c_i64, c_ptr, c_ptr]),
     "wg_sorted_offsets": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),

@@ -6,18 +6,19 @@ any partition of the particle index space yields the bitwise-identical
 raster (the reference's own thread-invariance contract, simulate.py:449-453,
 489-503).
 
-Partition: the grid's rows are cut into ``nranks * bands_per_rank`` bands
-(whole tiles tall); band b belongs to rank b % nranks (cyclic, so terrain
-that is steep in one region spreads over all ranks).  A rank simulates the
+Partition: the grid's rows are cut into about ``nranks * bands_per_rank``
+bands of a power-of-two number of rows (whole tiles); band b belongs to rank
+b % nranks (cyclic, so terrain that is steep in one region spreads over all
+ranks).  A rank simulates the
 particles released in its bands -- release cells are numbered row-major, so
 a band's particles are one contiguous range of the global particle index,
 and a rank's share is a few ranges (csrc/traj.cu ``ranges``).
 
 Merge: a particle travels ~80 cells, so a rank's visits stay in and near its
-own bands.  The trajectory kernel marks every tile (64 x 64 cells) a visit
-lands in; after the run each rank packs only its touched tiles that lie in
-other ranks' bands, one NCCL all-to-all moves them to their owners, and the
-owners add / max them into their rasters (csrc/merge.cu).  The owners' bands
+own bands.  The trajectory kernel marks every tile (64 x 64 cells) of
+another rank's bands that a visit lands in; after the run each rank packs
+those tiles, one NCCL all-to-all moves them to their owners, and the owners
+add / max them into their rasters (csrc/merge.cu).  The owners' bands
 then hold the exact single-GPU raster; nothing else moves.  ``gather_bands``
 gives every rank the whole raster (the reference API's result) when a caller
 needs it.  Under the gloo backend (CPU tests, several ranks on one GPU) the
@@ -44,8 +45,12 @@ class BandPlan:
     nrows: int
     ncols: int
     nranks: int
-    band_rows: int
+    band_rows: int  # a power of two, a multiple of the tile height
     tile_log2: int = TILE_LOG2
+
+    @property
+    def band_log2(self) -> int:
+        return self.band_rows.bit_length() - 1
 
     @property
     def nbands(self) -> int:
@@ -85,9 +90,11 @@ class BandPlan:
 
 def plan_bands(nrows: int, ncols: int, nranks: int, bands_per_rank: int = BANDS_PER_RANK,
                tile_log2: int = TILE_LOG2) -> BandPlan:
-    t = 1 << tile_log2
+    """Bands of the smallest power-of-two height (>= one tile) that makes at
+    most nranks * bands_per_rank of them."""
     per = -(-nrows // (nranks * bands_per_rank))
-    return BandPlan(nrows, ncols, nranks, max(t, -(-per // t) * t), tile_log2)
+    rows = 1 << max(tile_log2, (per - 1).bit_length())
+    return BandPlan(nrows, ncols, nranks, rows, tile_log2)
 
 
 def particle_ranges(cell_offsets: list[int], plan: BandPlan, rank: int, per_cell: int) -> list[tuple[int, int]]:
@@ -156,8 +163,9 @@ def touched_tiles(touched: torch.Tensor) -> tuple[torch.Tensor, int]:
 
 
 def pack_foreign(hits: torch.Tensor, zmax: torch.Tensor, touched: torch.Tensor, plan: BandPlan, rank: int):
-    """(counts, ids, data): this rank's touched tiles in other ranks' bands,
-    grouped by destination rank; data holds a 2*T*T-word block per tile."""
+    """(counts, ids, data): this rank's touched tiles (all in other ranks'
+    bands), grouped by destination rank; data holds a 2*T*T-word block per
+    tile."""
     from . import _lib
 
     L = _lib.lib()
@@ -187,11 +195,16 @@ def accumulate_tiles(hits: torch.Tensor, zmax: torch.Tensor, plan: BandPlan, ids
                                      _lib.ptr(ids), ids.numel(), _lib.ptr(data), _lib.stream_ptr()))
 
 
-def clear_tiles(hits: torch.Tensor, zmax: torch.Tensor, touched: torch.Tensor, plan: BandPlan) -> None:
-    """Zero the touched tiles of both rasters and the touched map (reuse of
-    persistent rasters without a full-raster memset)."""
+def clear_tiles(hits: torch.Tensor, zmax: torch.Tensor, touched: torch.Tensor, plan: BandPlan, rank: int) -> None:
+    """Make a rank's rasters zero again for the next run without a
+    full-raster memset: its own bands (1/N of the raster) and the foreign
+    tiles it touched; then the touched map."""
     from . import _lib
 
+    for b in plan.owned_bands(rank):
+        r0, r1 = plan.rows(b)
+        hits[r0:r1].zero_()
+        zmax[r0:r1].zero_()
     ids, n = touched_tiles(touched)
     if n:
         L = _lib.lib()
@@ -320,8 +333,8 @@ def run_sharded(grid, cells: torch.Tensor, params, group=None, plan: BandPlan | 
     if touched is None:
         touched = _device.zeros((plan.tiles_y, plan.tiles_x), torch.uint8)
     ranges = particle_ranges(band_cell_offsets(cells, plan), plan, rank, params.particles_per_release_cell)
-    run_avalanche_device(grid, cells, params, ranges=ranges, hits=hits, zmax=zmax, touched=touched,
-                         tile_log2=plan.tile_log2)
+    run_avalanche_device(grid, cells, params, ranges=ranges, hits=hits, zmax=zmax, touched=touched, plan=plan,
+                         rank=rank)
     traffic = merge_tiles(hits, zmax, touched, plan, group)
     return ShardedRun(hits, zmax, touched, plan, ranges, traffic)
 

@@ -493,12 +493,15 @@ def run_avalanche_device(
     hits: torch.Tensor | None = None,
     zmax: torch.Tensor | None = None,
     touched: torch.Tensor | None = None,
-    tile_log2: int = 6,
+    plan=None,
+    rank: int = 0,
     stream: torch.cuda.Stream | None = None,
 ) -> tuple[torch.Tensor, torch.Tensor]:
     """Launch the trajectory kernel over the particles [i_lo, i_hi) (or the
     ascending disjoint `ranges`, a rank's bands) accumulating into (hits,
-    zmax) and, when given, the touched-tile map; no host sync."""
+    zmax); with `touched` (and the shard.BandPlan `plan`, this being `rank`)
+    also marking the tiles of other ranks' bands its visits land in.  No
+    host sync."""
     L = _lib.lib()
     sc = kernel_scalars(grid, params)
     total = int(cells.numel()) * params.particles_per_release_cell
@@ -511,6 +514,8 @@ def run_avalanche_device(
         zmax = _device.zeros((grid.nrows, grid.ncols), torch.float64)
     if all(b <= a for a, b in ranges):
         return hits, zmax
+    if touched is not None and (plan is None or plan.nranks < 2):
+        touched = None  # one rank: no other rank's bands to mark
     span_lo, span_hi = ranges[0][0], ranges[-1][1]
     scratch = _device.empty((int(L.wg_avalanche_scratch_bytes(params.particles_per_release_cell, span_lo,
                                                                span_hi)),), torch.uint8)
@@ -521,7 +526,8 @@ def run_avalanche_device(
         L.wg_run_avalanche(
             _lib.ptr(dem), _lib.ptr(quad), _lib.ptr(pair), *_sc_args(sc), _lib.ptr(cells),
             params.particles_per_release_cell, rng.seed_word(params.seed), pairs, len(ranges), _lib.ptr(absmax),
-            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(touched), int(tile_log2), _lib.ptr(scratch),
+            _lib.ptr(hits), _lib.ptr(zmax), _lib.ptr(touched), plan.tile_log2 if plan else 0,
+            plan.band_log2 if plan else 0, int(rank), plan.nranks if plan else 1, _lib.ptr(scratch),
             _lib.stream_ptr(stream),
         ),
         ParamError,

@@ -79,7 +79,7 @@ def test_c5_two_rank_bands_equal_one_rank(c5):
         zmax.zero_()
         touched.zero_()
         run_avalanche_device(grid, cells, params, ranges=shard.particle_ranges(offs, plan, r, PPC), hits=hits,
-                             zmax=zmax, touched=touched, tile_log2=plan.tile_log2)
+                             zmax=zmax, touched=touched, plan=plan, rank=r)
 
     # rank 1's tiles in rank 0's bands, then rank 0 with them folded in
     run_rank(1)

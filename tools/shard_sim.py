@@ -65,7 +65,7 @@ def main() -> None:
             touched.zero_()
             ranges = shard.particle_ranges(offs, plan, r, 2048)
             ms = timed(lambda: run_avalanche_device(grid, cells, params, ranges=ranges, hits=hits, zmax=zmax,
-                                                    touched=touched, tile_log2=plan.tile_log2))
+                                                    touched=touched, plan=plan, rank=r))
             particles = shard.local_particles(ranges)
             steps = int(hits.sum().item()) - particles
             ids, nt = shard.touched_tiles(touched)
