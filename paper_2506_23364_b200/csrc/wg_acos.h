@@ -20,7 +20,7 @@
 #include "wg_fp64.h"
 
 #if defined(__CUDA_ARCH__) || defined(__CUDACC__)
-#define WG_ACOS_TABLE static __device__ const
+#define WG_ACOS_TABLE static __device__ const __align__(16)
 #else
 #define WG_ACOS_TABLE static const
 #endif
@@ -36,28 +36,18 @@ WG_HD double wg_rsqrt14(double s) {
   if ((u & 0x000fffffffffffffULL) == 0 && (e & 1) == 0) return wg_from_bits((uint64_t)(1023 - e / 2) << 52);
   const uint32_t par = (uint32_t)e & 1u;
   const uint32_t idx = (par << 15) | (uint32_t)((u >> 37) & 0x7fffu);
-  const uint32_t g = idx >> 5, k = idx & 31u;
+  const uint32_t g = idx >> 3, k = idx & 7u;
+  // record g: (value of entry 0, nibble word of backward differences)
 #if defined(__CUDA_ARCH__)
-  const uint4 w = __ldg(reinterpret_cast<const uint4*>(wg_rsq14_nib) + g);
-  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-  const uint32_t base = __ldg(wg_rsq14_base + g);
+  const uint2 rec = __ldg(reinterpret_cast<const uint2*>(wg_rsq14_tab) + g);
+  const uint32_t base = rec.x, word = rec.y;
 #else
-  const uint32_t* words = wg_rsq14_nib + 4 * g;
-  const uint32_t base = wg_rsq14_base[g];
+  const uint32_t base = wg_rsq14_tab[2 * g], word = wg_rsq14_tab[2 * g + 1];
 #endif
-  // sum of nibbles 1..k of the group (nibble 0 is zero): word j holds
-  // entries 8j..8j+7
-  uint32_t tot = 0;
-#if defined(__CUDACC__)
-#pragma unroll
-#endif
-  for (int j = 0; j < 4; j++) {
-    const int c = (int)k - 8 * j + 1;  // nibbles of this word that count
-    const uint32_t m = c >= 8 ? 0xffffffffu : (c <= 0 ? 0u : ((1u << (4 * c)) - 1u));
-    const uint32_t x = words[j] & m;
-    const uint32_t b = (x & 0x0f0f0f0fu) + ((x >> 4) & 0x0f0f0f0fu);
-    tot += (b * 0x01010101u) >> 24;
-  }
+  // sum of nibbles 1..k (nibble 0 is zero): mask, then a SWAR byte sum
+  const uint32_t x = word & (k == 7u ? 0xffffffffu : ((1u << (4 * (k + 1))) - 1u));
+  const uint32_t b = (x & 0x0f0f0f0fu) + ((x >> 4) & 0x0f0f0f0fu);
+  const uint32_t tot = (b * 0x01010101u) >> 24;
   const int q = par ? -16 - (e + 1) / 2 : -17 - e / 2;
   return (double)(int)(base - tot) * wg_from_bits((uint64_t)(q + 1023) << 52);
 }
