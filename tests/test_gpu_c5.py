@@ -10,7 +10,9 @@ multi-GPU config, checked on one B200:
   tiles packed and folded into their owners (the data the NCCL all-to-all
   moves) -- gives every band of its owner the 1-rank raster bit for bit
   (per-band device digests);
-* 16 evenly spaced 2048-particle chunks equal the C oracle bit for bit.
+* 16 evenly spaced 2048-particle chunks equal the C oracle bit for bit
+  (stop reasons, steps, end points), and so does the whole run's raster
+  (every particle, ~2 minutes of the oracle on the box's host threads).
 
 HBM: DEM 32 GiB + rasters 64 GiB (+ the packed tiles); the gather layout is
 held at the plain DEM here (the bench uses the 64 GiB row-pair layout)."""
@@ -120,3 +122,38 @@ def test_c5_sampled_chunks_equal_oracle(c5):
                                             particles_per_release_cell=PPC, seed=SEED, records=True)
         assert np.array_equal(rr, orr) and np.array_equal(st, ost), int(c)
         assert np.array_equal(en.view(np.int64), oen.view(np.int64)), int(c)
+
+
+def test_c5_full_raster_equals_oracle(c5):
+    """Every particle of C5 (2.2e8 particles, 1.09e10 steps), GPU vs the C
+    oracle on the box's host threads (~2 minutes); compared band by band on
+    the device (the host holds the 32 GiB DEM and the oracle's 64 GiB of
+    rasters)."""
+    import os
+
+    from oracle import traj
+
+    from paper_2506_23364_b200.simulate import run_avalanche_device
+
+    wf, grid, mask, cells, params = c5
+    hits = torch.zeros((N, N), dtype=torch.int64, device="cuda")
+    zmax = torch.zeros((N, N), dtype=torch.float64, device="cuda")
+    run_avalanche_device(grid, cells, params, hits=hits, zmax=zmax)
+    elev = grid.elevations
+    cells_h = cells.cpu().numpy().astype(np.int64)
+    oh = np.zeros((N, N), dtype=np.int64)
+    oz = np.zeros((N, N), dtype=np.float64)
+    total = cells_h.size * PPC
+    steps = traj.run_range(elev, 0.0, 0.0, 10.0, cells_h, 0, total, oh, oz, particles_per_release_cell=PPC, seed=SEED,
+                           threads=os.cpu_count())
+    assert steps > 1.0e10
+    rows = 2048
+    bh = torch.empty((rows, N), dtype=torch.int64, device="cuda")
+    bz = torch.empty((rows, N), dtype=torch.float64, device="cuda")
+    bad_h = bad_z = 0
+    for r0 in range(0, N, rows):
+        bh.copy_(torch.from_numpy(oh[r0:r0 + rows]))
+        bz.copy_(torch.from_numpy(oz[r0:r0 + rows]))
+        bad_h += int((hits[r0:r0 + rows] != bh).sum().item())
+        bad_z += int((zmax[r0:r0 + rows].view(torch.int64) != bz.view(torch.int64)).sum().item())
+    assert bad_h == 0 and bad_z == 0, (bad_h, bad_z)
