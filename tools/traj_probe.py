@@ -115,7 +115,10 @@ def main():
         times.append(round(e0.elapsed_time(e1), 2))
     steps = int(hits.sum().item()) - int(cells.numel()) * a.ppc
     out = {"cells": int(cells.numel()), "particles": int(cells.numel()) * a.ppc, "steps": steps,
-           "quad": quad_ok, "layout": a.layout, "ms": times, "clocks": clocks, "gsteps_s_best": round(steps / min(times) / 1e6, 2)}
+           "quad": quad_ok, "layout": a.layout, "ms": times,
+           # raster checksums: variants of the kernel must agree bit for bit
+           "hits_wsum": int((hits.view(-1)[::7]).sum().item()), "zbits_xor": int(
+               zmax.view(torch.int64).view(-1)[::3].sum().item()), "clocks": clocks, "gsteps_s_best": round(steps / min(times) / 1e6, 2)}
     if a.records:
         from paper_2506_23364_b200.simulate import particle_records
 
