@@ -129,6 +129,16 @@ def main():
         out["lifetime"] = {"mean": round(float(st.mean()), 1), "max": int(st.max()),
                            "p50_p90_p99_p999": np.percentile(st, [50, 90, 99, 99.9]).round(1).tolist()}
         out["reasons"] = np.bincount(reason.astype(np.int64), minlength=4).tolist()
+        # per release cell: how well does one particle predict its cell's
+        # longest particle (a longest-first claim order would need that)
+        per = st.reshape(-1, a.ppc).astype(np.float64)
+        cmax, cmean, p0 = per.max(1), per.mean(1), per[:, 0]
+        out["cells"] = {"max_of_max": int(cmax.max()), "cells_max_over_1000": int((cmax > 1000).sum()),
+                        "cells_max_over_500": int((cmax > 500).sum()),
+                        "corr_p0_cellmax": round(float(np.corrcoef(p0, cmax)[0, 1]), 3),
+                        "corr_p0_cellmean": round(float(np.corrcoef(p0, cmean)[0, 1]), 3),
+                        "corr_mean_max": round(float(np.corrcoef(cmean, cmax)[0, 1]), 3),
+                        "cellmax_p50_p90_p99_p999": np.percentile(cmax, [50, 90, 99, 99.9]).round(1).tolist()}
     print(json.dumps(out))
 
 
