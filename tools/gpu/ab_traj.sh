@@ -7,7 +7,7 @@ for round in 1 2; do
 for v in ${BUILDS}; do
   rm -f paper_2506_23364_b200/_lib/obj/traj.o
   make -C $C -j8 NVCC_EXTRA="${v//,/ }" >/dev/null 2>&1 || { echo "build $v failed"; continue; }
-  timeout 600 python tools/traj_probe.py --reps ${REPS:-6} > gpurun_out/ab.log 2>gpurun_out/ab.err; grep -h "traj timing" gpurun_out/ab.err | tail -2 >> gpurun_out/ab_timing.txt
+  timeout 600 python tools/traj_probe.py --reps ${REPS:-6} ${PROBE_ARGS:-} > gpurun_out/ab.log 2>gpurun_out/ab.err; grep -h "traj timing" gpurun_out/ab.err | tail -2 >> gpurun_out/ab_timing.txt
   echo "$round $v $(python -c "
 import json,statistics as st
 d=json.loads(open('gpurun_out/ab.log').read().strip().splitlines()[-1])
