@@ -77,13 +77,19 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--records", action="store_true", help="also report particle lifetime stats")
     ap.add_argument("--layout", choices=["auto", "pair", "dem"], default="auto", help="force the gather layout")
+    ap.add_argument("--lattice", action="store_true", help="release mask from the DEM at lattice cells (C5: no slope field)")
     a = ap.parse_args()
     _lib.build()
     elev = synth_dem_device(a.size, a.seed)
-    grid = wf.DemGrid(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, elev)
+    grid = wf.DemGrid.adopt(a.size, a.size, 0.0, 0.0, 10.0, -9999.0, elev)
     params = wf.AvalancheParams(particles_per_release_cell=a.ppc, seed=a.seed)
-    _, slope = compute_normals_and_slope(grid)
-    mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
+    if a.lattice:
+        from paper_2506_23364_b200.simulate import release_mask_from_dem
+
+        mask = release_mask_from_dem(grid, 30.0, 45.0, a.stride)
+    else:
+        _, slope = compute_normals_and_slope(grid)
+        mask = wf.detect_release_points(slope, 30.0, 45.0, a.stride)
     cells = release_cells(mask)
     hits = torch.zeros((a.size, a.size), dtype=torch.int64, device="cuda")
     zmax = torch.zeros((a.size, a.size), dtype=torch.float64, device="cuda")
