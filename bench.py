@@ -66,9 +66,6 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlay", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--serial", action="store_true",
-                    help="N = 1: one step after another on one stream (default: two streams, a step's "
-                         "upstream and trajectory launch queued while the previous step drains)")
     ap.add_argument("--config", choices=["c3", "c5"], default="c3",
                     help="c3: 16384^2 stride 32 (default, BASELINE configs[2]); "
                          "c5: 65536^2 stride 128 seed 2 (configs[4]; lattice-slope mask prefix, no e2e/CPU legs)")
@@ -320,10 +317,6 @@ def main() -> None:
         total_hits, cells, _, _, traffic = hot_path(grid)
     released = int(cells.numel()) * params.particles_per_release_cell
     total_steps = total_hits - released
-    pipe_bufs = None
-    if world == 1 and not a.serial:
-        pipe_bufs = [(torch.empty((a.size, a.size), dtype=torch.int64, device=dev),
-                      torch.empty((a.size, a.size), dtype=torch.float64, device=dev)) for _ in range(2)]
 
     # timed: device-resident
     barrier()
@@ -333,42 +326,10 @@ def main() -> None:
     with Clocks(local) as clk:
         t0.record(stream)
         evs, mevs = [], []
-        if world == 1 and not a.serial:
-            # Two streams, each with its own raster pair: step i's normals /
-            # mask / cells and its trajectory launch are queued while step
-            # i-1's launch drains (the GPU fills the drain tail with the next
-            # step's work), and step i-1's stats are read after that.  Every
-            # step is complete inside [t0, t1].
-            streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
-            for st2 in streams:
-                st2.wait_event(t0)
-            pending = None
-            for i in range(a.steps):
-                st2 = streams[i % 2]
-                hits, zmax = pipe_bufs[i % 2]
-                with torch.cuda.stream(st2):
-                    cells = upstream(grid)
-                    hits.zero_()
-                    zmax.zero_()
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(st2)
-                    run_avalanche_device(grid, cells, params, hits=hits, zmax=zmax)
-                    e1.record(st2)
-                evs.append((e0, e1))
-                mevs.append(None)
-                if pending is not None:
-                    with torch.cuda.stream(pending[0]):
-                        assert wf.RunoutRaster(pending[2], pending[1]).total_hits == total_hits
-                pending = (st2, hits, zmax)
-            with torch.cuda.stream(pending[0]):
-                assert wf.RunoutRaster(pending[2], pending[1]).total_hits == total_hits
-            for st2 in streams:
-                stream.wait_stream(st2)
-        else:
-            for _ in range(a.steps):
-                _, cells, ev, mev, traffic = hot_path(grid)
-                evs.append(ev)
-                mevs.append(mev)
+        for _ in range(a.steps):
+            _, cells, ev, mev, traffic = hot_path(grid)
+            evs.append(ev)
+            mevs.append(mev)
         t1.record(stream)
         barrier()
     launches = _lib.launch_count() - launches0
@@ -420,9 +381,6 @@ def main() -> None:
             "parallelism": (f"release-row bands over {world} GPUs ({plan.nbands} bands of {plan.band_rows} rows, "
                             f"cyclic), touched-tile all-to-all merge to the band owners ({backend})"
                             if world > 1 else "1 GPU"),
-            "schedule": ("serial: one step after another on one stream" if (world > 1 or a.serial) else
-                         "two CUDA streams: a step's normals / mask / cells and its trajectory launch are queued "
-                         "while the previous step's launch drains; every step completes inside the timed region"),
             "particle_steps_per_step": total_steps,
             "released_particles": released,
             "traj_kernel_ms": traj_avg,
