@@ -9,6 +9,9 @@
 //   red_max  : one 8-byte RED.MAX.64 per op                   -- the drop max
 //   step     : gather32 + red_add + red_max per op, the three to the same
 //              kind of slots the trajectory step touches (a memory-only step)
+//   *_red    : the same with the reductions issued as PTX red (REDG) instead
+//              of atomicAdd / atomicMax with an unused result (ATOMG to RZ) --
+//              what the trajectory kernel uses
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2_peak l2_peak.cu
 #include <cstdio>
 #include <cstdint>
@@ -37,6 +40,13 @@ __global__ void __launch_bounds__(128, 8) probe(const double* __restrict__ quad,
     }
     if (kMode == 1 || kMode == 3) atomicAdd(hits + slot, 1ULL);
     if (kMode == 2 || kMode == 3) atomicMax(zmax + slot, h >> 12);
+    if (kMode == 4 || kMode == 6) asm volatile("red.global.add.u64 [%0], 1;" ::"l"(hits + slot) : "memory");
+    if (kMode == 5 || kMode == 6) asm volatile("red.global.max.u64 [%0], %1;" ::"l"(zmax + slot), "l"(h >> 12) : "memory");
+    if (kMode == 6) {
+      double a, b, c, d;
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(quad + 4 * slot));
+      acc += a + b + c + d;
+    }
   }
   if (acc == 1.2345) sink[0] = acc;
 }
@@ -58,8 +68,8 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int blocks = sms * 8, iters = 4096;
   const double ops = (double)blocks * 128 * iters;
-  const char* names[4] = {"gather32", "red_add", "red_max", "step"};
-  for (int mode = 0; mode < 4; mode++) {
+  const char* names[7] = {"gather32", "red_add", "red_max", "step", "red_add_red", "red_max_red", "step_red"};
+  for (int mode = 0; mode < 7; mode++) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -70,7 +80,10 @@ int main() {
         case 0: probe<0><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
         case 1: probe<1><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
         case 2: probe<2><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
-        default: probe<3><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
+        case 3: probe<3><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
+        case 4: probe<4><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
+        case 5: probe<5><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
+        default: probe<6><<<blocks, 128>>>(quad, hits, zmax, nslots, iters, sink); break;
       }
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
@@ -79,7 +92,7 @@ int main() {
       if (rep > 0 && ms < best) best = ms;  // rep 0 warms L2
     }
     const double per_s = ops / (best * 1e-3);
-    const double bytes = mode == 0 ? 32.0 : mode == 3 ? 64.0 : 16.0;  // atomics: 8-B read + 8-B write
+    const double bytes = mode == 0 ? 32.0 : (mode == 3 || mode == 6) ? 64.0 : 16.0;  // atomics: 8-B read + 8-B write
     printf("{\"probe\": \"%s\", \"ops_per_s\": %.4e, \"gb_s\": %.1f, \"ms\": %.3f, \"sms\": %d, \"working_set_mib\": 96}\n",
            names[mode], per_s, per_s * bytes / 1e9, best, sms);
   }
