@@ -42,12 +42,12 @@ BYTES_PER_STEP = 64  # 32 B DEM patch + 16 B hit RMW + 16 B drop
 # FP64-pipe instructions per particle-step (DFMA+DMUL+DADD+DSETP per active
 # thread) from the ncu SASS capture of traj_kernel (profiles/r01_traj_ncu_summary.txt),
 # and the measured FP64 instruction peak (profiles/fp64_peak.json, DADD/DMUL rate)
-FP64_OPS_PER_STEP = 167  # 143 DFMA+DMUL+DADD + 24 DSETP (ncu source page, round-2 final build)
+FP64_OPS_PER_STEP = 168  # 143 DFMA+DMUL+DADD + 25 DSETP (ncu source page, round-2 final build)
 FP64_PEAK_OPS = 1.853e13
 # the step's memory operations alone (one 32-B gather + RED.ADD.64 + RED.MAX.64
 # to random slots of a 96 MiB L2-resident working set, 32 warps/SM): the L2
 # access-rate ceiling of a trajectory step (tools/micro/l2_peak.cu, profiles/l2_peak.json)
-L2_STEP_PEAK = 6.6177e10
+L2_STEP_PEAK = 6.7024e10
 # DRAM bytes per traj_kernel launch from ncu --set full (dram__bytes_read+write, r01)
 TRAJ_DRAM_BYTES = 6.60e9
 

@@ -90,8 +90,11 @@ __global__ void accumulate_kernel(unsigned long long* __restrict__ hits, unsigne
       if (r >= g.nrows || c >= g.ncols) continue;
       const int64_t cell = r * g.ncols + c;
       const unsigned long long h = src[q], z = src[cells + q];
-      if (h) atomicAdd(hits + cell, h);
-      if (z) atomicMax(zbits + cell, z);  // drops are >= +0.0: bit order == value order
+      // reductions with unused results as PTX red (REDG: cheaper than an
+      // atomic to RZ in the trajectory kernel); drops are >= +0.0, so bit
+      // order is value order
+      if (h) asm volatile("red.global.add.u64 [%0], %1;" ::"l"(hits + cell), "l"(h) : "memory");
+      if (z) asm volatile("red.global.max.u64 [%0], %1;" ::"l"(zbits + cell), "l"(z) : "memory");
     }
   }
 }
